@@ -1,0 +1,186 @@
+/*
+ * lz.h -- C-ABI of liblz.so, the B200 (sm_100a) hot path of the Lazarus MoE layer
+ * (arXiv 2407.04656): gating -> replica-split planning -> pack -> [all-to-all]
+ * -> grouped expert FFN -> [all-to-all] -> combine, plus the backward kernels.
+ *
+ * The reference (flexep 0.1.0, pure Python) exposes the dispatcher as Python
+ * functions; this header is the FFI a maintainer binds in their place (see
+ * INTEGRATION.md for the ctypes stub).  Each entry point cites the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/flexep).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless stated; every call is asynchronous
+ *     on `stream` (a cudaStream_t passed as void*), caller owns all memory,
+ *     the library keeps no device state between calls (stateless, re-entrant);
+ *   - T[e*N + j]  tokens routed to expert e originating on rank j  (E x N)
+ *     R[e*N + j]  replicas of expert e on rank j, COMMUNICATOR-rank order (E x N)
+ *     D[(i*E + e)*N + j] tokens of expert e sent by rank i to rank j (N x E x N)
+ *   - routed assignments are flattened token-major: p = t*k + s;
+ *   - bf16 tensors are row-major with the model dimension contiguous;
+ *   - data-dependent errors (e.g. tokens routed to an expert without replicas)
+ *     are reported through `err` (device int32 bit set, LZ_ERRF_*); the host reads
+ *     it at its next synchronisation point and raises the reference's exception.
+ */
+#ifndef LZ_H_
+#define LZ_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LZ_OK = 0,
+  LZ_ERR_ARG = 1,        /* host-side argument / shape error   (reference: ValueError)          */
+  LZ_ERR_UNROUTABLE = 2, /* reserved for synchronous variants  (reference: UnroutableTokenError) */
+  LZ_ERR_CUDA = 3,       /* CUDA launch / runtime error                                          */
+  LZ_ERR_WORKSPACE = 4,  /* workspace too small                                                   */
+  LZ_ERR_UNSUPPORTED = 5 /* shape outside the compiled limits                                     */
+} lz_status;
+
+/* device error-flag bits written into `err` */
+#define LZ_ERRF_UNROUTABLE 1  /* t_e > 0 and r_e == 0          dispatch.py:147-150 */
+#define LZ_ERRF_COUNTS 2      /* routed list disagrees with T  dispatch.py:213-229 */
+#define LZ_ERRF_EXPERT_ID 4   /* routed expert id out of range dispatch.py:220-222 */
+
+/* compiled limits */
+#define LZ_MAX_RANKS 64
+#define LZ_MAX_EXPERTS 1024
+#define LZ_MAX_EN 4096 /* E*N */
+#define LZ_MAX_TOPK 8
+
+const char* lz_status_string(int status);
+int lz_version(void);
+int lz_last_cuda_error(void); /* cudaError_t of the last failed call on this thread */
+
+/* ---------------------------------------------------------------- K2 planning */
+
+/* Replaces full_dispatch_matrices (dispatch.py:129-159) + the quota computation
+ * (dispatch.py:143-151): quota[E] (int64) and D for ALL senders, bit-exact with the
+ * reference (largest-remainder split core.py:321-341, ties to the lower rank). */
+lz_status lz_plan_matrices(const int32_t* T, const int32_t* R, int E, int N, int64_t* quota,
+                           int32_t* D, int32_t* err, void* stream);
+
+/* Workspace needed by lz_plan_dispatch for (E, N, P). */
+lz_status lz_plan_workspace_bytes(int E, int N, int P, size_t* bytes);
+
+/* Replaces compute_dispatch_schedule (dispatch.py:162-196) for `rank` plus
+ * build_shuffle_index (dispatch.py:199-237) and invert_permutation (:240-244):
+ *   quota[E], D[N*E*N]                   as lz_plan_matrices
+ *   send_sizes[N]                        s_j incl. self                    (dispatch.py:178-180)
+ *   recv_sizes[N]                        reference convention, self = 0    (dispatch.py:181-184)
+ *   recv_counts[N]                       NCCL convention, self = D[r][*][r]
+ *   slot[P]   send-buffer position of local assignment p (= invert_permutation(index))
+ *   gather[P] local assignment at send slot s            (= build_shuffle_index result)
+ *   dest_row[P] row of assignment p in its destination rank's expert-major receive
+ *             buffer (segments padded to `align` rows, source-major inside an expert)
+ *   recv_m[E]        tokens of expert e this rank receives (incl. self)   (received[j][e][:] sum, :276-282)
+ *   recv_off[E+1]    padded expert-major offsets of this rank's receive buffer
+ *   recv_src_off[E*N] row where source i's tokens of expert e start on this rank
+ *   recv_stage_off[E*N], recv_cnt[E*N] (optional, both or neither): where the
+ *             (source i, expert e) segment sits in a plain all-to-all receive buffer
+ *             (source-major, expert-major inside) and its length D[i][e][rank]
+ * `routed` may be NULL (P = 0) to compute counts only.  Errors -> `err`. */
+lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E, int N, int rank,
+                           const int32_t* routed, int P, int align, int64_t* quota, int32_t* D,
+                           int32_t* send_sizes, int32_t* recv_sizes, int32_t* recv_counts,
+                           int32_t* slot, int32_t* gather, int32_t* dest_row, int32_t* recv_m,
+                           int32_t* recv_off, int32_t* recv_src_off, int32_t* recv_stage_off,
+                           int32_t* recv_cnt, int32_t* err, void* ws, size_t ws_bytes,
+                           void* stream);
+
+/* Replaces build_shuffle_index (dispatch.py:199-237) given only a schedule's
+ * send_counts (E x N, = DispatchSchedule.send_counts): slot[P] and gather[P] as above;
+ * validation errors (dispatch.py:213-229) -> `err`. ws as lz_plan_workspace_bytes. */
+lz_status lz_shuffle_index(const int32_t* send_counts, int E, int N, const int32_t* routed, int P,
+                           int32_t* slot, int32_t* gather, int32_t* err, void* ws,
+                           size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------- K1 gating */
+
+/* softmax over E logits, top-k (ties -> lower expert id), weights = top-k probs
+ * (renorm = 0) or renormalised over the k (renorm = 1), per-rank expert
+ * histogram hist[E] = T[:, rank] (the gather_load_matrix input, dispatch.py:95-107).
+ * logits fp32 [Tn, E]. probs (fp32 [Tn, E]) may be NULL. */
+lz_status lz_gate_topk(const float* logits, int Tn, int E, int k, int renorm, int32_t* idx,
+                       float* w, float* probs, int32_t* hist, void* stream);
+
+/* Fused router: logits = x[Tn, d] (bf16) . wg[E, d]^T (bf16) + bias[E] (fp32, may be
+ * NULL), fp32 accumulate, then as lz_gate_topk.  d % 32 == 0, E <= 64. */
+lz_status lz_router_gate(const void* x, const void* wg, const float* bias, int Tn, int d, int E,
+                         int k, int renorm, int32_t* idx, float* w, float* probs, int32_t* hist,
+                         void* stream);
+
+/* Replaces invert_permutation (dispatch.py:240-244): out[index[i]] = i. */
+lz_status lz_invert_permutation(const int32_t* index, int n, int32_t* out, void* stream);
+
+/* ----------------------------------------------------------- K3 pack / regroup */
+
+/* out[row[t*k+s]] = x[t] (bf16 rows of d elements; d % 8 == 0).  When E > 0 the
+ * padding rows of the expert-major layout (recv_m, recv_off) are zero-filled. */
+lz_status lz_pack(const void* x, int Tn, int d, int k, const int32_t* row, void* out, int E,
+                  const int32_t* recv_m, const int32_t* recv_off, void* stream);
+
+/* Row-segment copy: for every segment g, rows [src[g], src[g]+cnt[g]) of `in` go to
+ * rows [dst[g], ...) of `out` (regroups an all-to-all receive buffer into the
+ * expert-major GEMM layout and back).  nseg segments, all arrays device int32. */
+lz_status lz_copy_segments(const void* in, void* out, int d, int nseg, const int32_t* src,
+                           const int32_t* dst, const int32_t* cnt, int max_cnt, void* stream);
+
+/* ------------------------------------------------------------------ K7 combine */
+
+/* out[t] = sum_s w[t,s] * y[row[t*k+s]]  (fixed s order, fp32 accumulate, bf16 out). */
+lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, int d, int k,
+                     void* out, void* stream);
+
+/* -------------------------------------------------------------- K8 backward */
+
+/* dy[row[t,s]] = w[t,s] * dout[t];  dw[t,s] = <dout[t], y[row[t,s]]>  (fp32).
+ * Padding rows of the expert-major layout are zero-filled when E > 0. */
+lz_status lz_combine_bwd(const void* dout, const void* y, const int32_t* row, const float* w,
+                         int Tn, int d, int k, void* dy, float* dw, int E, const int32_t* recv_m,
+                         const int32_t* recv_off, void* stream);
+
+/* Gate backward + dispatch backward, fused per token:
+ *   dlogits[t,:] from probs, idx, dw (softmax/top-k(/renorm) backward)
+ *   dx[t] = sum_s dxe[row[t,s]] + dlogits[t,:] . wg        (wg bf16 [E, d]; may be NULL) */
+lz_status lz_dispatch_bwd(const void* dxe, const int32_t* row, int Tn, int d, int k,
+                          const float* probs, const int32_t* idx, const float* dw,
+                          const void* wg, int E, int renorm, void* dx, float* dlogits,
+                          void* stream);
+
+/* Router weight gradient: dwg[E, d] (fp32) = dlogits^T . x ; dbias[E] = sum_t dlogits.
+ * ws >= lz_router_wgrad_ws_bytes(). */
+size_t lz_router_wgrad_ws_bytes(int Tn, int d, int E);
+lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, int E, float* dwg,
+                          float* dbias, void* ws, size_t ws_bytes, void* stream);
+
+/* ----------------------------------------------------- K4-K6 grouped expert GEMM */
+
+/* Epilogues */
+#define LZ_EPI_STORE 0     /* C = acc (bf16)                                   */
+#define LZ_EPI_GELU 1      /* C = gelu(acc), AUX = acc (pre-activation, bf16)  */
+#define LZ_EPI_DGELU 2     /* C = acc * gelu'(AUX)                             */
+/* Operand majors */
+#define LZ_K_MAJOR 0
+#define LZ_MN_MAJOR 1
+
+/* Grouped GEMM on tcgen05/TMEM (TMA-fed, persistent, warp-specialised).
+ * Groups g = 0..G-1 are described by the device array off[G+1] (row offsets,
+ * every segment a multiple of 128 rows):
+ *   mode 0 ("rows"):   C[off[g]:off[g+1], :N] = A[off[g]:off[g+1], :K] . B_g
+ *                      A K-major [rows, K]; B_g = B[g*N:(g+1)*N, :K] (b_major = K) or
+ *                      B[g*K:(g+1)*K, :N] (b_major = MN)
+ *   mode 1 ("wgrad"):  C_g[M, N] = A[off[g]:off[g+1], :M]^T . B[off[g]:off[g+1], :N]
+ *                      (both MN-major, variable K = segment length, C at C + g*M*N)
+ * M, N, K multiples of 128 / 256 / 64 as documented in DESIGN.md. */
+lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux, int G,
+                          const int32_t* off, int rows_total, int M, int N, int K, int b_major,
+                          int epilogue, int num_sms, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LZ_H_ */

@@ -1,0 +1,108 @@
+"""ctypes binding of liblz.so (include/lz.h).  There is no fallback: if the
+library is missing or fails to load, every entry point raises."""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_DIR, "liblz.so")
+
+_vp, _i, _sz, _fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p
+
+# name -> argtypes (restype int status unless listed in _RESTYPE)
+_SIGS = {
+    "lz_status_string": [_i],
+    "lz_version": [],
+    "lz_last_cuda_error": [],
+    "lz_plan_matrices": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp],
+    "lz_plan_workspace_bytes": [_i, _i, _i, ctypes.POINTER(ctypes.c_size_t)],
+    # T R E N rank routed P align | quota D send recv recv_counts slot gather dest_row
+    # recv_m recv_off recv_src_off recv_stage_off recv_cnt err ws | ws_bytes stream
+    "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i] + [_vp] * 15 + [_sz, _vp],
+    "lz_shuffle_index": [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp],
+    "lz_gate_topk": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "lz_router_gate": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "lz_invert_permutation": [_vp, _i, _vp, _vp],
+    "lz_pack": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
+    "lz_copy_segments": [_vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp],
+    "lz_combine": [_vp, _vp, _vp, _i, _i, _i, _vp, _vp],
+    "lz_combine_bwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
+    "lz_dispatch_bwd": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp, _vp],
+    "lz_router_wgrad_ws_bytes": [_i, _i, _i],
+    "lz_router_wgrad": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _sz, _vp],
+    "lz_grouped_gemm": [_i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _vp],
+}
+_RESTYPE = {"lz_status_string": ctypes.c_char_p, "lz_router_wgrad_ws_bytes": ctypes.c_size_t}
+
+# header constants (include/lz.h)
+LZ_OK, LZ_ERR_ARG, LZ_ERR_UNROUTABLE, LZ_ERR_CUDA, LZ_ERR_WORKSPACE, LZ_ERR_UNSUPPORTED = range(6)
+LZ_ERRF_UNROUTABLE, LZ_ERRF_COUNTS, LZ_ERRF_EXPERT_ID = 1, 2, 4
+LZ_EPI_STORE, LZ_EPI_GELU, LZ_EPI_DGELU = 0, 1, 2
+LZ_K_MAJOR, LZ_MN_MAJOR = 0, 1
+LZ_MAX_RANKS, LZ_MAX_EXPERTS, LZ_MAX_EN, LZ_MAX_TOPK = 64, 1024, 4096, 8
+
+
+class LzError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: {msg} (status {status})")
+        self.status = status
+
+
+_lock = threading.Lock()
+_handle = None
+
+
+def load() -> ctypes.CDLL:
+    """Load liblz.so once.  Raises if it is absent: the product has no CPU path."""
+    global _handle
+    if _handle is not None:
+        return _handle
+    with _lock:
+        if _handle is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} not found: build it with `python -m paper_2407_04656_b200.build` "
+                    "(the Lazarus B200 path has no CPU fallback)")
+            h = ctypes.CDLL(LIB_PATH)
+            for name, args in _SIGS.items():
+                fn = getattr(h, name)
+                fn.argtypes = args
+                fn.restype = _RESTYPE.get(name, ctypes.c_int)
+            _handle = h
+    return _handle
+
+
+def exported_symbols() -> list[str]:
+    return list(_SIGS)
+
+
+def call(name: str, *args) -> None:
+    h = load()
+    st = getattr(h, name)(*args)
+    if st != LZ_OK:
+        msg = h.lz_status_string(st).decode()
+        if st == LZ_ERR_CUDA:
+            msg += f" (cudaError {h.lz_last_cuda_error()})"
+        if st == LZ_ERR_ARG:
+            raise ValueError(f"{name}: {msg}")
+        raise LzError(name, st, msg)
+
+
+def raw(name: str, *args):
+    return getattr(load(), name)(*args)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None passes NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

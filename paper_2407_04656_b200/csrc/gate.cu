@@ -1,0 +1,227 @@
+// gate.cu -- K1: gating softmax / top-k (+ fused router GEMM) and per-rank histogram.
+//
+// No reference code exists for this stage; semantics are
+// restated from PAPER.md:94-95 ("a trainable gate network routes each token to
+// only the top-k experts") with the reference's tie rule (lower id wins, as in
+// allocation.py:94, placement.py:131, core.py:339).  Selection is done on the
+// fp32 logits (exact), so the routed expert ids are bit-exact against the CPU
+// oracle for identical logits; probabilities/weights carry fp32 rounding only.
+//
+// hist[e] is this rank's column T[:, rank] of the load matrix that the
+// all-gather assembles (gather_load_matrix, dispatch.py:95-107).
+#include "common.cuh"
+
+namespace lz {
+
+// Softmax + top-k for one token whose E logits are at `lg` (smem or global).
+__device__ __forceinline__ void finish_token(const float* lg, int E, int k, int renorm,
+                                             int32_t* __restrict__ idx_out,
+                                             float* __restrict__ w_out,
+                                             float* __restrict__ probs_out,
+                                             int32_t* s_hist) {
+  int sel[LZ_MAX_TOPK];
+  float sv[LZ_MAX_TOPK];
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s) {
+    sel[s] = -1;
+    sv[s] = -INFINITY;
+  }
+  float mx = -INFINITY;
+  for (int e = 0; e < E; ++e) {
+    const float v = lg[e];
+    mx = fmaxf(mx, v);
+    // insertion into the running top-k: strictly greater wins, so ties keep the lower id
+    if (v > sv[k - 1] || sel[k - 1] < 0) {
+      int pos = k - 1;
+      while (pos > 0 && (v > sv[pos - 1] || sel[pos - 1] < 0)) {
+        sv[pos] = sv[pos - 1];
+        sel[pos] = sel[pos - 1];
+        --pos;
+      }
+      sv[pos] = v;
+      sel[pos] = e;
+    }
+  }
+  float sum = 0.f;
+  for (int e = 0; e < E; ++e) sum += expf(lg[e] - mx);
+  const float inv = 1.f / sum;
+  if (probs_out)
+    for (int e = 0; e < E; ++e) probs_out[e] = expf(lg[e] - mx) * inv;
+  float ps[LZ_MAX_TOPK];
+  float psum = 0.f;
+  for (int s = 0; s < k; ++s) {
+    ps[s] = expf(sv[s] - mx) * inv;
+    psum += ps[s];
+  }
+  const float rn = renorm ? 1.f / psum : 1.f;
+  for (int s = 0; s < k; ++s) {
+    idx_out[s] = sel[s];
+    w_out[s] = ps[s] * rn;
+    atomicAdd(&s_hist[sel[s]], 1);
+  }
+}
+
+__global__ void __launch_bounds__(256) gate_topk_kernel(const float* __restrict__ logits, int Tn,
+                                                        int E, int k, int renorm,
+                                                        int32_t* __restrict__ idx,
+                                                        float* __restrict__ w,
+                                                        float* __restrict__ probs,
+                                                        int32_t* __restrict__ hist) {
+  extern __shared__ int32_t s_hist[];
+  for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < Tn)
+    finish_token(logits + (size_t)t * E, E, k, renorm, idx + (size_t)t * k, w + (size_t)t * k,
+                 probs ? probs + (size_t)t * E : nullptr, s_hist);
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
+}
+
+// ---------------------------------------------------------------------------
+// Fused router: logits[t, :] = x[t, :] . wg^T + bias, on the legacy mma.sync
+// bf16 path (16 tokens x 8 experts per instruction; E <= 64 is far below the
+// tcgen05 tile width, and the stage is bound by reading x from HBM).
+// Each warp owns 16 tokens; lane (g = lane/4, t = lane%4) loads 16 contiguous
+// bytes of rows g and g+8 per 32-wide k chunk.  The k order inside a chunk is
+// permuted identically for A and B, which leaves the dot products unchanged.
+// ---------------------------------------------------------------------------
+constexpr int kRouterWarps = 8;
+constexpr int kRouterTok = 16 * kRouterWarps;
+
+__device__ __forceinline__ void mma_bf16_16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                               uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+template <int NT>
+__global__ void __launch_bounds__(32 * kRouterWarps) router_gate_kernel(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int Tn, int d, int E, int k, int renorm,
+    int32_t* __restrict__ idx, float* __restrict__ w, float* __restrict__ probs,
+    int32_t* __restrict__ hist) {
+  constexpr int EP = NT * 8 + 1;  // padded logit row (bank spread)
+  __shared__ float s_log[kRouterWarps][16][EP];
+  __shared__ int32_t s_hist[NT * 8];
+  for (int e = threadIdx.x; e < NT * 8; e += blockDim.x) s_hist[e] = 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = lane >> 2, tq = lane & 3;
+  const int tok0 = blockIdx.x * kRouterTok + warp * 16;
+  const int r0 = tok0 + g, r1 = tok0 + g + 8;
+  const bool v0 = r0 < Tn, v1 = r1 < Tn;
+  const __nv_bfloat16* x0 = x + (size_t)(v0 ? r0 : 0) * d + 8 * tq;
+  const __nv_bfloat16* x1 = x + (size_t)(v1 ? r1 : 0) * d + 8 * tq;
+  const __nv_bfloat16* wrow[NT];
+  bool wv[NT];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int e = nt * 8 + g;
+    wv[nt] = e < E;
+    wrow[nt] = wg + (size_t)(wv[nt] ? e : 0) * d + 8 * tq;
+  }
+  float acc[NT][4];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+  const uint4 zero = make_uint4(0, 0, 0, 0);
+  constexpr int U = 4;  // k chunks in flight
+  for (int kb = 0; kb < d; kb += 32 * U) {
+    uint4 xa[U], xb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + 32 * u;
+      xa[u] = (v0 && kk < d) ? ld_nc_v4(x0 + kk) : zero;
+      xb[u] = (v1 && kk < d) ? ld_nc_v4(x1 + kk) : zero;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int kk = kb + 32 * u;
+      if (kk >= d) break;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const uint4 bw = wv[nt] ? ld_v4(wrow[nt] + kk) : zero;
+        mma_bf16_16816(acc[nt], xa[u].x, xb[u].x, xa[u].y, xb[u].y, bw.x, bw.y);
+        mma_bf16_16816(acc[nt], xa[u].z, xb[u].z, xa[u].w, xb[u].w, bw.z, bw.w);
+      }
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int c0 = nt * 8 + 2 * tq;
+    const float b0 = (bias && c0 < E) ? bias[c0] : 0.f;
+    const float b1 = (bias && c0 + 1 < E) ? bias[c0 + 1] : 0.f;
+    s_log[warp][g][c0] = acc[nt][0] + b0;
+    s_log[warp][g][c0 + 1] = acc[nt][1] + b1;
+    s_log[warp][g + 8][c0] = acc[nt][2] + b0;
+    s_log[warp][g + 8][c0 + 1] = acc[nt][3] + b1;
+  }
+  __syncthreads();
+  if (lane < 16) {
+    const int t = tok0 + lane;
+    if (t < Tn)
+      finish_token(&s_log[warp][lane][0], E, k, renorm, idx + (size_t)t * k, w + (size_t)t * k,
+                   probs ? probs + (size_t)t * E : nullptr, s_hist);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
+}
+
+}  // namespace lz
+
+using namespace lz;
+
+extern "C" lz_status lz_gate_topk(const float* logits, int Tn, int E, int k, int renorm,
+                                  int32_t* idx, float* w, float* probs, int32_t* hist,
+                                  void* stream) {
+  if (Tn < 0 || E < 1 || E > LZ_MAX_EXPERTS || k < 1 || k > LZ_MAX_TOPK || k > E || !hist)
+    return LZ_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess) return lzh::check_launch();
+  if (Tn == 0) return LZ_OK;
+  if (!logits || !idx || !w) return LZ_ERR_ARG;
+  gate_topk_kernel<<<(Tn + 255) / 256, 256, sizeof(int32_t) * E, s>>>(logits, Tn, E, k, renorm,
+                                                                     idx, w, probs, hist);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* bias, int Tn,
+                                    int d, int E, int k, int renorm, int32_t* idx, float* w,
+                                    float* probs, int32_t* hist, void* stream) {
+  if (Tn < 0 || d < 32 || d % 32 || E < 1 || E > 64 || k < 1 || k > LZ_MAX_TOPK || k > E ||
+      !hist)
+    return LZ_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess) return lzh::check_launch();
+  if (Tn == 0) return LZ_OK;
+  if (!x || !wg || !idx || !w) return LZ_ERR_ARG;
+  const int grid = (Tn + kRouterTok - 1) / kRouterTok;
+  const auto* xb = (const __nv_bfloat16*)x;
+  const auto* wb = (const __nv_bfloat16*)wg;
+  const int NT = (E + 7) / 8;
+#define LZ_ROUTER_CASE(n)                                                                    \
+  case n:                                                                                    \
+    router_gate_kernel<n><<<grid, 32 * kRouterWarps, 0, s>>>(xb, wb, bias, Tn, d, E, k,       \
+                                                             renorm, idx, w, probs, hist);   \
+    break;
+  switch (NT) {
+    LZ_ROUTER_CASE(1)
+    LZ_ROUTER_CASE(2)
+    LZ_ROUTER_CASE(3)
+    LZ_ROUTER_CASE(4)
+    LZ_ROUTER_CASE(5)
+    LZ_ROUTER_CASE(6)
+    LZ_ROUTER_CASE(7)
+    LZ_ROUTER_CASE(8)
+    default:
+      return LZ_ERR_UNSUPPORTED;
+  }
+#undef LZ_ROUTER_CASE
+  return lzh::check_launch();
+}

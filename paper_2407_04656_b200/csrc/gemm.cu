@@ -1,0 +1,494 @@
+// gemm.cu -- K4/K5/K6: grouped expert GEMMs on 5th-gen tensor cores (sm_100a).
+//
+// One persistent, warp-specialised kernel serves every FFN GEMM of the layer:
+//   mode 0 (rows)  : per expert g, C[rows_g] = A[rows_g] . B_g      (fwd, dgrad)
+//   mode 1 (wgrad) : per expert g, C_g = A[rows_g]^T . B[rows_g]    (variable-K weight grad)
+// Tile 128 x 256 x 64 (bf16), UMMA 128x256x16 (kind::f16, fp32 accumulate in TMEM),
+// 4-stage TMA -> smem ring (128B swizzle), double-buffered TMEM accumulator
+// (2 x 256 columns) so the epilogue of tile i overlaps the main loop of tile i+1.
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma)
+//   warps 2..5  epilogue: tcgen05.ld 32x32b -> fused activation -> bf16 -> global
+// The reference has no FFN code; semantics follow PAPER.md:143
+// (one weight copy per (expert, rank); R[e][j] > 1 only scales capacity).
+#include <cuda.h>  // CUtensorMap (header only; the encoder is fetched at run time)
+
+#include "common.cuh"
+
+namespace lz {
+namespace gemm {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kStages = 4;
+constexpr int kThreads = 192;
+constexpr int kATileBytes = BM * BK * 2;  // 16 KB
+constexpr int kBTileBytes = BN * BK * 2;  // 32 KB
+constexpr int kStageBytes = kATileBytes + kBTileBytes;
+constexpr int kAccCols = BN;              // fp32 accumulator columns per buffer
+constexpr int kTmemCols = 2 * kAccCols;   // 512
+constexpr int kMaxGroups = 1024;
+constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+#ifndef LZ_NO_WATCHDOG
+  // a pipeline bug must fail loudly, not hang the GPU: trap after ~10 s of waiting
+  const long long t0 = clock64();
+#endif
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+#ifndef LZ_NO_WATCHDOG
+    if (!done && clock64() - t0 > 20000000000ll) __trap();
+#endif
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+
+// UMMA shared-memory descriptor (sm_100): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 [46,48), layout type [61,64) (2 = 128B swizzle).
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N>>3, M>>4.
+__host__ __device__ constexpr uint32_t make_idesc(int a_mn, int b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// tanh-approximate GELU ("gelu_new", GPT-2 MLP) and its derivative.
+__device__ __forceinline__ float tanh_fast(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kS2PI = 0.7978845608028654f;
+constexpr float kGC = 0.044715f;
+__device__ __forceinline__ float gelu_f(float x) {
+  const float u = kS2PI * fmaf(kGC * x, x * x, x);
+  return 0.5f * x * (1.f + tanh_fast(u));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+  const float x2 = x * x;
+  const float t = tanh_fast(kS2PI * fmaf(kGC * x, x2, x));
+  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * kS2PI * fmaf(3.f * kGC, x2, 1.f);
+}
+
+struct Params {
+  int mode;         // 0 rows, 1 wgrad
+  int G;            // groups
+  int M, N, K;      // mode 0: N, K used; mode 1: M, N
+  const int32_t* off;
+  __nv_bfloat16* C;
+  __nv_bfloat16* aux;
+  int epilogue;
+};
+
+// A tile load (128 x 64) for the current stage
+template <int A_MN>
+__device__ __forceinline__ void load_a(const CUtensorMap* map, uint8_t* dst, uint64_t* bar,
+                                       int row_or_k, int m0, int k0) {
+  if (A_MN == 0) {
+    tma_load_2d(dst, map, bar, k0, row_or_k);  // K-major: (k, row)
+  } else {
+    // MN-major: two 64-wide M boxes of 64 k-rows
+    tma_load_2d(dst, map, bar, m0, row_or_k);
+    tma_load_2d(dst + 8192, map, bar, m0 + 64, row_or_k);
+  }
+}
+template <int B_MN>
+__device__ __forceinline__ void load_b(const CUtensorMap* map, uint8_t* dst, uint64_t* bar,
+                                       int n_row, int n0, int k_row, int k0) {
+  if (B_MN == 0) {
+    tma_load_2d(dst, map, bar, k0, n_row);  // K-major (k, n-row)
+  } else {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(dst + 8192 * q, map, bar, n0 + 64 * q, k_row);
+  }
+}
+
+struct TileInfo {
+  int g, mb, nb, nk;
+};
+
+__device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
+                                                const int32_t* s_off, int tile) {
+  // binary search the group: s_pref[g] <= tile < s_pref[g+1]
+  int lo = 0, hi = p.G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (s_pref[mid] <= tile) lo = mid;
+    else hi = mid - 1;
+  }
+  TileInfo t;
+  t.g = lo;
+  const int local = tile - s_pref[lo];
+  const int nbn = p.N / BN;
+  t.mb = local / nbn;
+  t.nb = local % nbn;
+  t.nk = (p.mode == 0) ? p.K / BK : (s_off[lo + 1] - s_off[lo]) / BK;
+  return t;
+}
+
+template <int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
+                        const __grid_constant__ CUtensorMap map_b, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* s_tiles = smem;
+  uint64_t* full_bar = (uint64_t*)(smem + kStages * kStageBytes);
+  uint64_t* empty_bar = full_bar + kStages;
+  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* s_tmem = (uint32_t*)(tempty_bar + 2);
+  __shared__ int32_t s_off[kMaxGroups + 1];
+  __shared__ int32_t s_pref[kMaxGroups + 1];
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  // group table -> tile prefix (every CTA computes it; G <= 1024)
+  for (int g = threadIdx.x; g <= p.G; g += blockDim.x) s_off[g] = p.off[g];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    const int nbn = p.N / BN;
+    for (int g = 0; g < p.G; ++g) {
+      s_pref[g] = acc;
+      acc += (p.mode == 0) ? ((s_off[g + 1] - s_off[g]) / BM) * nbn : (p.M / BM) * nbn;
+    }
+    s_pref[p.G] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *s_tmem;
+  const int total = s_pref[p.G];
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+        for (int kb = 0; kb < t.nk; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = s_tiles + stage * kStageBytes;
+          uint8_t* sb = sa + kATileBytes;
+          mbar_expect_tx(&full_bar[stage], kStageBytes);
+          if (p.mode == 0) {
+            const int row = s_off[t.g] + t.mb * BM;
+            load_a<A_MN>(&map_a, sa, &full_bar[stage], row, 0, kb * BK);
+            load_b<B_MN>(&map_b, sb, &full_bar[stage], t.g * p.N + t.nb * BN, t.nb * BN,
+                         t.g * p.K + kb * BK, kb * BK);
+          } else {
+            const int krow = s_off[t.g] + kb * BK;
+            load_a<A_MN>(&map_a, sa, &full_bar[stage], krow, t.mb * BM, 0);
+            load_b<B_MN>(&map_b, sb, &full_bar[stage], 0, t.nb * BN, krow, 0);
+          }
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+        const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int kb = 0; kb < t.nk; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(s_tiles + stage * kStageBytes);
+          const uint32_t sb = sa + kATileBytes;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: +32 B per 16-element k step inside the 128 B swizzle atom
+            // MN-major: +2 x (8 rows x 128 B) per 16 k rows; atoms along MN are 8 KB apart
+            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024)
+                                     : make_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024)
+                                     : make_desc(sb + k * 32, 16, 1024);
+            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+          }
+          tc_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
+          if (++stage == kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+  } else {
+    // ===== epilogue warps 2..5 =====
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int r = quad * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
+      const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+      long row;
+      __nv_bfloat16* cbase;
+      __nv_bfloat16* abase = nullptr;
+      if (p.mode == 0) {
+        row = (long)s_off[t.g] + t.mb * BM + r;
+        cbase = p.C + row * p.N + t.nb * BN;
+        if (p.aux) abase = p.aux + row * p.N + t.nb * BN;
+      } else {
+        row = (long)t.mb * BM + r;
+        cbase = p.C + (long)t.g * p.M * p.N + row * p.N + t.nb * BN;
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        if (t.nk > 0) {
+          tmem_ld32(taddr + c * 32, v);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = 0u;
+        }
+        float f[32];
+#pragma unroll
+        for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+        uint4* dst = reinterpret_cast<uint4*>(cbase + c * 32);
+        if (p.epilogue == LZ_EPI_GELU) {
+          uint4* adst = reinterpret_cast<uint4*>(abase + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st_v4(adst + q, f32_to_bf16x8(f + 8 * q));
+#pragma unroll
+          for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
+        } else if (p.epilogue == LZ_EPI_DGELU) {
+          const uint4* hsrc = reinterpret_cast<const uint4*>(abase + c * 32);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float h[8];
+            bf16x8_to_f32(ld_nc_v4(hsrc + q), h);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) st_v4(dst + q, f32_to_bf16x8(f + 8 * q));
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty_bar[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace gemm
+}  // namespace lz
+
+// ------------------------------------------------------------------------ host
+using namespace lz::gemm;
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2D bf16 tensor map over a row-major [outer, inner] matrix, 128B swizzle.
+static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                     uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = get_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int A_MN, int B_MN>
+static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
+                        cudaStream_t s) {
+  auto kern = grouped_gemm_kernel<A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
+        cudaSuccess)
+      return lzh::check_launch();
+    attr_set = true;
+  }
+  kern<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, p);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
+                                     int G, const int32_t* off, int rows_total, int M, int N,
+                                     int K, int b_major, int epilogue, int num_sms,
+                                     void* stream) {
+  if (G < 1 || G > kMaxGroups || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
+  if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DGELU) return LZ_ERR_ARG;
+  if ((epilogue != LZ_EPI_STORE) && (mode != 0 || !aux)) return LZ_ERR_ARG;
+  if (N <= 0 || N % BN) return LZ_ERR_UNSUPPORTED;
+  CUtensorMap ma, mb;
+  Params p{};
+  p.mode = mode;
+  p.G = G;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.off = off;
+  p.C = (__nv_bfloat16*)C;
+  p.aux = (__nv_bfloat16*)aux;
+  p.epilogue = epilogue;
+  cudaStream_t s = (cudaStream_t)stream;
+  int sms = num_sms > 0 ? num_sms : lzh::num_sms();
+  if (rows_total == 0 && mode == 0) return LZ_OK;
+  if (mode == 0) {
+    if (K <= 0 || K % BK) return LZ_ERR_UNSUPPORTED;
+    if (!make_map(&ma, A, K, rows_total, BK, BM)) return LZ_ERR_CUDA;
+    if (b_major == LZ_K_MAJOR) {
+      if (!make_map(&mb, B, K, (uint64_t)G * N, BK, BN)) return LZ_ERR_CUDA;
+    } else {
+      if (!make_map(&mb, B, N, (uint64_t)G * K, 64, BK)) return LZ_ERR_CUDA;
+    }
+    // upper bound of tiles = rows_total/BM * N/BN; the kernel reads the exact count
+    long tiles = (long)(rows_total / BM) * (N / BN);
+    int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
+    return b_major == LZ_K_MAJOR ? launch<0, 0>(ma, mb, p, grid, s)
+                                 : launch<0, 1>(ma, mb, p, grid, s);
+  } else if (mode == 1) {
+    if (M <= 0 || M % BM) return LZ_ERR_UNSUPPORTED;
+    const uint64_t rows = rows_total > 0 ? rows_total : 1;
+    if (!make_map(&ma, A, M, rows, 64, BK)) return LZ_ERR_CUDA;
+    if (!make_map(&mb, B, N, rows, 64, BK)) return LZ_ERR_CUDA;
+    long tiles = (long)G * (M / BM) * (N / BN);
+    int grid = (int)(tiles < sms ? tiles : sms);
+    return launch<1, 1>(ma, mb, p, grid, s);
+  }
+  return LZ_ERR_ARG;
+}

@@ -1,0 +1,493 @@
+// permute.cu -- K3 pack, K7 combine, K8 backward permutes, router weight grad.
+//
+// All of these are HBM-bound row movers: one warp per token row, 16-byte
+// vectorised coalesced loads/stores, 4 vectors in flight per lane, streaming
+// (L1::no_allocate) loads for read-once activations.  Reference semantics:
+//   pack     Alg. 1 reshuffle: token rows go to the send/receive
+//            slot the planner assigned (dispatch.py:199-237 gives the index only)
+//   combine  PAPER.md:99 weighted sum of the k expert outputs (fixed s order)
+#include "common.cuh"
+
+namespace lz {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kVec = 4;  // uint4 per lane in flight
+
+__device__ __forceinline__ void zero_pad_rows(void* out, int d, int E, const int32_t* recv_m,
+                                              const int32_t* recv_off, long item, long n_items,
+                                              int lane) {
+  // item enumerates (expert, pad row) pairs; pad rows are [off[e]+m[e], off[e+1])
+  (void)n_items;
+  const int nch = d / 8;
+  for (int e = 0; e < E; ++e) {
+    const long start = (long)recv_off[e] + recv_m[e];
+    const long cnt = (long)recv_off[e + 1] - start;
+    if (item < cnt) {
+      uint4* dst = reinterpret_cast<uint4*>(out) + (start + item) * nch;
+      for (int c = lane; c < nch; c += 32) st_v4(dst + c, make_uint4(0, 0, 0, 0));
+      return;
+    }
+    item -= cnt;
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) pack_kernel(
+    const uint4* __restrict__ x, int Tn, int d, int k, const int32_t* __restrict__ row,
+    uint4* __restrict__ out, int E, const int32_t* __restrict__ recv_m,
+    const int32_t* __restrict__ recv_off, long n_pad_items) {
+  const int lane = threadIdx.x % 32;
+  const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
+  const long nw = (long)gridDim.x * kRowWarps;
+  const int nch = d / 8;
+  for (long t = gw; t < Tn + n_pad_items; t += nw) {
+    if (t >= Tn) {
+      zero_pad_rows(out, d, E, recv_m, recv_off, t - Tn, n_pad_items, lane);
+      continue;
+    }
+    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const uint4* src = x + t * nch;
+    for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
+      uint4 v[kVec];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (c0 + 32 * u < nch) v[u] = ld_nc_v4(src + c0 + 32 * u);
+      for (int s = 0; s < k; ++s) {
+        const long r = __shfl_sync(0xffffffffu, my_row, s);
+        uint4* dst = out + r * nch;
+#pragma unroll
+        for (int u = 0; u < kVec; ++u)
+          if (c0 + 32 * u < nch) st_v4(dst + c0 + 32 * u, v[u]);
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) combine_kernel(const uint4* __restrict__ y,
+                                                              const int32_t* __restrict__ row,
+                                                              const float* __restrict__ w,
+                                                              int Tn, int d, int k,
+                                                              uint4* __restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
+  const long nw = (long)gridDim.x * kRowWarps;
+  const int nch = d / 8;
+  for (long t = gw; t < Tn; t += nw) {
+    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const float my_w = lane < k ? __ldg(w + t * k + lane) : 0.f;
+    for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
+      float acc[kVec][8];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+      for (int s = 0; s < k; ++s) {
+        const long r = __shfl_sync(0xffffffffu, my_row, s);
+        const float ws = __shfl_sync(0xffffffffu, my_w, s);
+        const uint4* src = y + r * nch;
+        uint4 v[kVec];
+#pragma unroll
+        for (int u = 0; u < kVec; ++u)
+          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(src + c0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+          if (c0 + 32 * u < nch) {
+            float f[8];
+            bf16x8_to_f32(v[u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[u][q] = fmaf(ws, f[q], acc[u][q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (c0 + 32 * u < nch) st_v4(out + t * nch + c0 + 32 * u, f32_to_bf16x8(acc[u]));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
+    const uint4* __restrict__ dout, const uint4* __restrict__ y, const int32_t* __restrict__ row,
+    const float* __restrict__ w, int Tn, int d, int k, uint4* __restrict__ dy,
+    float* __restrict__ dw, int E, const int32_t* __restrict__ recv_m,
+    const int32_t* __restrict__ recv_off, long n_pad_items) {
+  const int lane = threadIdx.x % 32;
+  const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
+  const long nw = (long)gridDim.x * kRowWarps;
+  const int nch = d / 8;
+  for (long t = gw; t < Tn + n_pad_items; t += nw) {
+    if (t >= Tn) {
+      zero_pad_rows(dy, d, E, recv_m, recv_off, t - Tn, n_pad_items, lane);
+      continue;
+    }
+    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const float my_w = lane < k ? __ldg(w + t * k + lane) : 0.f;
+    float dot[LZ_MAX_TOPK];
+#pragma unroll
+    for (int s = 0; s < LZ_MAX_TOPK; ++s) dot[s] = 0.f;
+    for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
+      float g[kVec][8];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (c0 + 32 * u < nch) bf16x8_to_f32(ld_nc_v4(dout + t * nch + c0 + 32 * u), g[u]);
+#pragma unroll
+      for (int s = 0; s < LZ_MAX_TOPK; ++s) {
+        if (s >= k) break;
+        const long r = __shfl_sync(0xffffffffu, my_row, s);
+        const float ws = __shfl_sync(0xffffffffu, my_w, s);
+        uint4 v[kVec];
+#pragma unroll
+        for (int u = 0; u < kVec; ++u)
+          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(y + r * nch + c0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+          if (c0 + 32 * u < nch) {
+            float f[8], o[8];
+            bf16x8_to_f32(v[u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              dot[s] = fmaf(g[u][q], f[q], dot[s]);
+              o[q] = ws * g[u][q];
+            }
+            st_v4(dy + r * nch + c0 + 32 * u, f32_to_bf16x8(o));
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < LZ_MAX_TOPK; ++s) {
+      if (s >= k) break;
+      const float tot = warp_sum(dot[s]);
+      if (lane == 0) dw[t * k + s] = tot;
+    }
+  }
+}
+
+// Gate backward (softmax + top-k (+renorm)) and dispatch backward, one warp per token.
+__global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
+    const uint4* __restrict__ dxe, const int32_t* __restrict__ row, int Tn, int d, int k,
+    const float* __restrict__ probs, const int32_t* __restrict__ idx,
+    const float* __restrict__ dwv, const uint4* __restrict__ wg, int E, int renorm,
+    uint4* __restrict__ dx, float* __restrict__ dlogits) {
+  const int lane = threadIdx.x % 32;
+  const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
+  const long nw = (long)gridDim.x * kRowWarps;
+  const int nch = d / 8;
+  for (long t = gw; t < Tn; t += nw) {
+    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const int my_idx = lane < k ? __ldg(idx + t * k + lane) : -1;
+    const float my_dw = lane < k ? __ldg(dwv + t * k + lane) : 0.f;
+    // lane owns experts e = lane and e = lane + 32 (E <= 64)
+    float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      if (e < E) p[h] = __ldg(probs + t * E + e);
+    }
+    // top-k probs and S for renorm
+    float S = 0.f, sum_dw_w = 0.f;
+    if (renorm) {
+      for (int s = 0; s < k; ++s) {
+        const int es = __shfl_sync(0xffffffffu, my_idx, s);
+        const float ps = __ldg(probs + t * E + es);
+        S += ps;
+      }
+      for (int s = 0; s < k; ++s) {
+        const int es = __shfl_sync(0xffffffffu, my_idx, s);
+        const float dws = __shfl_sync(0xffffffffu, my_dw, s);
+        sum_dw_w += dws * (__ldg(probs + t * E + es) / S);
+      }
+    }
+    for (int s = 0; s < k; ++s) {
+      const int es = __shfl_sync(0xffffffffu, my_idx, s);
+      const float dws = __shfl_sync(0xffffffffu, my_dw, s);
+      const float g = renorm ? (dws - sum_dw_w) / S : dws;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (es == lane + 32 * h) dp[h] += g;
+    }
+    const float pdp = warp_sum(p[0] * dp[0] + p[1] * dp[1]);
+    float dl[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int e = lane + 32 * h;
+      dl[h] = p[h] * (dp[h] - pdp);
+      if (e < E) dlogits[t * E + e] = dl[h];
+    }
+    for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
+      float acc[kVec][8];
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
+      for (int s = 0; s < k; ++s) {
+        const long r = __shfl_sync(0xffffffffu, my_row, s);
+        uint4 v[kVec];
+#pragma unroll
+        for (int u = 0; u < kVec; ++u)
+          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(dxe + r * nch + c0 + 32 * u);
+#pragma unroll
+        for (int u = 0; u < kVec; ++u) {
+          if (c0 + 32 * u < nch) {
+            float f[8];
+            bf16x8_to_f32(v[u], f);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[u][q] += f[q];
+          }
+        }
+      }
+      if (wg) {
+        for (int e = 0; e < E; ++e) {
+          const float de = __shfl_sync(0xffffffffu, dl[e >> 5], e & 31);
+#pragma unroll
+          for (int u = 0; u < kVec; ++u) {
+            if (c0 + 32 * u < nch) {
+              float f[8];
+              bf16x8_to_f32(__ldg(wg + (long)e * nch + c0 + 32 * u), f);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[u][q] = fmaf(de, f[q], acc[u][q]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kVec; ++u)
+        if (c0 + 32 * u < nch) st_v4(dx + t * nch + c0 + 32 * u, f32_to_bf16x8(acc[u]));
+    }
+  }
+}
+
+// dwg partials: block (bx, by, bz) reduces its token stripe for columns
+// [by*1024, +1024) and experts [bz*16, +16); thread owns 4 columns x 16 experts.
+constexpr int kWgE = 16;
+constexpr int kWgTokTile = 64;
+__global__ void __launch_bounds__(256) router_wgrad_partial(const float* __restrict__ dlog,
+                                                            const __nv_bfloat16* __restrict__ x,
+                                                            int Tn, int d, int E,
+                                                            float* __restrict__ part,
+                                                            float* __restrict__ part_bias) {
+  __shared__ float s_dl[kWgTokTile][kWgE];
+  const int nblk = gridDim.x;
+  const int col = blockIdx.y * 1024 + threadIdx.x * 4;
+  const int e0 = blockIdx.z * kWgE;
+  float acc[kWgE][4];
+#pragma unroll
+  for (int e = 0; e < kWgE; ++e)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[e][q] = 0.f;
+  float bacc = 0.f;
+  const long per = (Tn + nblk - 1) / nblk;
+  const long t_begin = (long)blockIdx.x * per;
+  const long t_end = min((long)Tn, t_begin + per);
+  for (long tt = t_begin; tt < t_end; tt += kWgTokTile) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < kWgTokTile * kWgE; q += blockDim.x) {
+      const int ti = q / kWgE, ei = q % kWgE;
+      const long t = tt + ti;
+      s_dl[ti][ei] = (t < t_end && e0 + ei < E) ? dlog[t * E + e0 + ei] : 0.f;
+    }
+    __syncthreads();
+    const int nt = (int)min((long)kWgTokTile, t_end - tt);
+    if (blockIdx.y == 0 && threadIdx.x < kWgE)
+      for (int ti = 0; ti < nt; ++ti) bacc += s_dl[ti][threadIdx.x];
+    if (col < d) {
+      for (int ti = 0; ti < nt; ++ti) {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + (tt + ti) * d + col));
+        const float x0 = __uint_as_float(raw.x << 16), x1 = __uint_as_float(raw.x & 0xffff0000u);
+        const float x2 = __uint_as_float(raw.y << 16), x3 = __uint_as_float(raw.y & 0xffff0000u);
+#pragma unroll
+        for (int e = 0; e < kWgE; ++e) {
+          const float g = s_dl[ti][e];
+          acc[e][0] = fmaf(g, x0, acc[e][0]);
+          acc[e][1] = fmaf(g, x1, acc[e][1]);
+          acc[e][2] = fmaf(g, x2, acc[e][2]);
+          acc[e][3] = fmaf(g, x3, acc[e][3]);
+        }
+      }
+    }
+  }
+  if (col < d) {
+#pragma unroll
+    for (int e = 0; e < kWgE; ++e) {
+      if (e0 + e < E) {
+        float4 v = make_float4(acc[e][0], acc[e][1], acc[e][2], acc[e][3]);
+        *reinterpret_cast<float4*>(part + ((long)blockIdx.x * E + e0 + e) * d + col) = v;
+      }
+    }
+  }
+  if (blockIdx.y == 0 && threadIdx.x < kWgE && e0 + threadIdx.x < E)
+    part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
+}
+
+__global__ void router_wgrad_reduce(const float* __restrict__ part,
+                                    const float* __restrict__ part_bias, int nblk, int d, int E,
+                                    float* __restrict__ dwg, float* __restrict__ dbias) {
+  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long n = (long)E * d;
+  if (i < n) {
+    float s = 0.f;
+    for (int b = 0; b < nblk; ++b) s += part[(long)b * n + i];
+    dwg[i] = s;
+  }
+  if (dbias && i < E) {
+    float s = 0.f;
+    for (int b = 0; b < nblk; ++b) s += part_bias[(long)b * E + i];
+    dbias[i] = s;
+  }
+}
+
+__global__ void copy_segments_kernel(const uint4* __restrict__ in, uint4* __restrict__ out, int d,
+                                     const int32_t* __restrict__ src,
+                                     const int32_t* __restrict__ dst,
+                                     const int32_t* __restrict__ cnt) {
+  const int g = blockIdx.y;
+  const int nch = d / 8;
+  const long n = cnt[g];
+  const long s0 = src[g], d0 = dst[g];
+  const long total = n * nch;
+  for (long q = (long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long)gridDim.x * blockDim.x) {
+    const long r = q / nch, c = q % nch;
+    st_v4(out + (d0 + r) * nch + c, ld_nc_v4(in + (s0 + r) * nch + c));
+  }
+}
+
+static int row_grid(long items) {
+  const long want = (items + kRowWarps - 1) / kRowWarps;
+  const long cap = (long)lzh::num_sms() * 16;  // 16 x 256-thread CTAs resident per SM max
+  return (int)(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+}  // namespace lz
+
+using namespace lz;
+
+static long pad_items(int E, const int32_t* recv_m, const int32_t* recv_off, int align_hint) {
+  (void)recv_m;
+  (void)recv_off;
+  return (long)E * align_hint;  // upper bound of pad rows handled per expert pass
+}
+
+// Pad rows are enumerated per expert inside zero_pad_rows; we launch enough warp
+// items to cover the worst case of (align-1) pad rows per expert, align = 128.
+static constexpr int kPadAlign = 128;
+
+extern "C" lz_status lz_pack(const void* x, int Tn, int d, int k, const int32_t* row, void* out,
+                             int E, const int32_t* recv_m, const int32_t* recv_off,
+                             void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
+  if (Tn > 0 && (!x || !row || !out)) return LZ_ERR_ARG;
+  if (E > 0 && (!recv_m || !recv_off || !out)) return LZ_ERR_ARG;
+  const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
+  if (Tn + npad == 0) return LZ_OK;
+  pack_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)x, Tn, d, k, row, (uint4*)out, E, recv_m, recv_off, npad);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, int d,
+                                int k, void* out, void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK) return LZ_ERR_ARG;
+  if (Tn == 0) return LZ_OK;
+  if (!y || !row || !w || !out) return LZ_ERR_ARG;
+  combine_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)y, row, w, Tn, d, k, (uint4*)out);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_combine_bwd(const void* dout, const void* y, const int32_t* row,
+                                    const float* w, int Tn, int d, int k, void* dy, float* dw,
+                                    int E, const int32_t* recv_m, const int32_t* recv_off,
+                                    void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
+  if (Tn > 0 && (!dout || !y || !row || !w || !dy || !dw)) return LZ_ERR_ARG;
+  if (E > 0 && (!recv_m || !recv_off || !dy)) return LZ_ERR_ARG;
+  const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
+  if (Tn + npad == 0) return LZ_OK;
+  combine_bwd_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dout, (const uint4*)y, row, w, Tn, d, k, (uint4*)dy, dw, E, recv_m, recv_off,
+      npad);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_dispatch_bwd(const void* dxe, const int32_t* row, int Tn, int d, int k,
+                                     const float* probs, const int32_t* idx, const float* dw,
+                                     const void* wg, int E, int renorm, void* dx,
+                                     float* dlogits, void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 1 || E > 64)
+    return LZ_ERR_ARG;
+  if (Tn == 0) return LZ_OK;
+  if (!dxe || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
+  dispatch_bwd_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dxe, row, Tn, d, k, probs, idx, dw, (const uint4*)wg, E, renorm, (uint4*)dx,
+      dlogits);
+  return lzh::check_launch();
+}
+
+static int wgrad_nblk(int Tn) {
+  int n = lzh::num_sms();
+  long per = (Tn + n - 1) / n;
+  if (per < 64) n = (Tn + 63) / 64;
+  return n < 1 ? 1 : n;
+}
+
+extern "C" size_t lz_router_wgrad_ws_bytes(int Tn, int d, int E) {
+  const size_t nblk = (size_t)wgrad_nblk(Tn);
+  return nblk * (size_t)E * d * sizeof(float) + nblk * (size_t)E * sizeof(float) + 256;
+}
+
+extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, int E,
+                                     float* dwg, float* dbias, void* ws, size_t ws_bytes,
+                                     void* stream) {
+  if (Tn < 0 || d <= 0 || d % 4 || E < 1 || !dwg) return LZ_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (Tn == 0) {
+    cudaMemsetAsync(dwg, 0, sizeof(float) * E * d, s);
+    if (dbias) cudaMemsetAsync(dbias, 0, sizeof(float) * E, s);
+    return lzh::check_launch();
+  }
+  if (!dlogits || !x || !ws) return LZ_ERR_ARG;
+  if (ws_bytes < lz_router_wgrad_ws_bytes(Tn, d, E)) return LZ_ERR_WORKSPACE;
+  const int nblk = wgrad_nblk(Tn);
+  float* part = (float*)ws;
+  float* part_bias = part + (size_t)nblk * E * d;
+  dim3 grid(nblk, (d + 1023) / 1024, (E + kWgE - 1) / kWgE);
+  router_wgrad_partial<<<grid, 256, 0, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
+                                            part_bias);
+  lz_status st = lzh::check_launch();
+  if (st != LZ_OK) return st;
+  const long n = (long)E * d;
+  router_wgrad_reduce<<<(int)((n + 255) / 256), 256, 0, s>>>(part, part_bias, nblk, d, E, dwg,
+                                                             dbias);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_copy_segments(const void* in, void* out, int d, int nseg,
+                                      const int32_t* src, const int32_t* dst, const int32_t* cnt,
+                                      int max_cnt, void* stream) {
+  if (d <= 0 || d % 8 || nseg < 0 || max_cnt < 0) return LZ_ERR_ARG;
+  if (nseg == 0 || max_cnt == 0) return LZ_OK;
+  if (!in || !out || !src || !dst || !cnt) return LZ_ERR_ARG;
+  const long per = (long)max_cnt * (d / 8);
+  int gx = (int)((per + 255) / 256);
+  if (gx > 1024) gx = 1024;
+  dim3 grid(gx, nseg);
+  copy_segments_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const uint4*)in, (uint4*)out, d,
+                                                               src, dst, cnt);
+  return lzh::check_launch();
+}
+
+__global__ void invert_permutation_kernel(const int32_t* __restrict__ index, int n,
+                                          int32_t* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[__ldg(index + i)] = i;
+}
+
+extern "C" lz_status lz_invert_permutation(const int32_t* index, int n, int32_t* out,
+                                           void* stream) {
+  if (n < 0) return LZ_ERR_ARG;
+  if (n == 0) return LZ_OK;
+  if (!index || !out) return LZ_ERR_ARG;
+  invert_permutation_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(index, n, out);
+  return lzh::check_launch();
+}

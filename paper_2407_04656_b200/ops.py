@@ -1,0 +1,147 @@
+"""Thin torch-tensor wrappers over the liblz C-ABI kernels (include/lz.h).
+
+Every function launches on the current CUDA stream, allocates its outputs with the
+torch caching allocator and never synchronises.  No CPU path exists: a missing
+library or a non-CUDA tensor raises.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+from ._lib import ptr
+
+ALIGN = 128  # expert segments of the receive buffer are padded to the GEMM M tile
+
+
+def _s():
+    return _lib.stream_ptr()
+
+
+def _cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise ValueError("liblz kernels take CUDA tensors only")
+
+
+def router_gate(x, wg, bias, k: int, renorm: bool = False, probs: bool = True):
+    """logits = x . wg^T + bias (fp32 acc) -> softmax/top-k.  Returns idx [T,k] int32,
+    w [T,k] fp32, probs [T,E] fp32 (or None), hist [E] int32."""
+    _cuda(x, wg, bias)
+    Tn, d = x.shape
+    E = wg.shape[0]
+    dev = x.device
+    idx = torch.empty((Tn, k), dtype=torch.int32, device=dev)
+    w = torch.empty((Tn, k), dtype=torch.float32, device=dev)
+    pr = torch.empty((Tn, E), dtype=torch.float32, device=dev) if probs else None
+    hist = torch.empty(E, dtype=torch.int32, device=dev)
+    _lib.call("lz_router_gate", ptr(x), ptr(wg), ptr(bias), Tn, d, E, k, int(renorm), ptr(idx),
+              ptr(w), ptr(pr), ptr(hist), _s())
+    return idx, w, pr, hist
+
+
+def gate_topk(logits, k: int, renorm: bool = False):
+    _cuda(logits)
+    Tn, E = logits.shape
+    dev = logits.device
+    idx = torch.empty((Tn, k), dtype=torch.int32, device=dev)
+    w = torch.empty((Tn, k), dtype=torch.float32, device=dev)
+    pr = torch.empty((Tn, E), dtype=torch.float32, device=dev)
+    hist = torch.empty(E, dtype=torch.int32, device=dev)
+    _lib.call("lz_gate_topk", ptr(logits.float().contiguous()), Tn, E, k, int(renorm), ptr(idx),
+              ptr(w), ptr(pr), ptr(hist), _s())
+    return idx, w, pr, hist
+
+
+def pack(x, row, k: int, out, recv_m=None, recv_off=None):
+    """out[row[t*k+s]] = x[t]; zero-fills the padding rows when recv_m/recv_off given."""
+    _cuda(x, row, out)
+    Tn, d = x.shape
+    E = 0 if recv_m is None else recv_m.numel()
+    _lib.call("lz_pack", ptr(x), Tn, d, k, ptr(row), ptr(out), E, ptr(recv_m), ptr(recv_off),
+              _s())
+    return out
+
+
+def zero_pad_rows(buf, recv_m, recv_off):
+    d = buf.shape[1]
+    _lib.call("lz_pack", None, 0, d, 1, None, ptr(buf), recv_m.numel(), ptr(recv_m),
+              ptr(recv_off), _s())
+
+
+def copy_segments(src_buf, dst_buf, src_off, dst_off, cnt, max_cnt: int):
+    d = src_buf.shape[1]
+    _lib.call("lz_copy_segments", ptr(src_buf), ptr(dst_buf), d, cnt.numel(), ptr(src_off),
+              ptr(dst_off), ptr(cnt), int(max_cnt), _s())
+    return dst_buf
+
+
+def combine(y, row, w, k: int, out=None):
+    _cuda(y, row, w)
+    Tn = w.shape[0]
+    d = y.shape[1]
+    if out is None:
+        out = torch.empty((Tn, d), dtype=torch.bfloat16, device=y.device)
+    _lib.call("lz_combine", ptr(y), ptr(row), ptr(w), Tn, d, k, ptr(out), _s())
+    return out
+
+
+def combine_bwd(dout, y, row, w, k: int, dy, recv_m=None, recv_off=None):
+    """dy[row[t,s]] = w[t,s] dout[t] (pads zeroed); returns dw [T,k] fp32."""
+    _cuda(dout, y, row, w, dy)
+    Tn, d = dout.shape
+    dw = torch.empty((Tn, k), dtype=torch.float32, device=dout.device)
+    E = 0 if recv_m is None else recv_m.numel()
+    _lib.call("lz_combine_bwd", ptr(dout), ptr(y), ptr(row), ptr(w), Tn, d, k, ptr(dy), ptr(dw),
+              E, ptr(recv_m), ptr(recv_off), _s())
+    return dw
+
+
+def dispatch_bwd(dxe, row, probs, idx, dw, wg, renorm: bool, Tn: int):
+    _cuda(dxe, row, probs, idx, dw, wg)
+    d = dxe.shape[1]
+    k = idx.shape[1]
+    E = probs.shape[1]
+    dx = torch.empty((Tn, d), dtype=torch.bfloat16, device=dxe.device)
+    dlog = torch.empty((Tn, E), dtype=torch.float32, device=dxe.device)
+    _lib.call("lz_dispatch_bwd", ptr(dxe), ptr(row), Tn, d, k, ptr(probs), ptr(idx), ptr(dw),
+              ptr(wg), E, int(renorm), ptr(dx), ptr(dlog), _s())
+    return dx, dlog
+
+
+def router_wgrad(dlogits, x, with_bias: bool = True):
+    _cuda(dlogits, x)
+    Tn, d = x.shape
+    E = dlogits.shape[1]
+    dwg = torch.empty((E, d), dtype=torch.float32, device=x.device)
+    db = torch.empty(E, dtype=torch.float32, device=x.device) if with_bias else None
+    nbytes = int(_lib.raw("lz_router_wgrad_ws_bytes", Tn, d, E))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=x.device)
+    _lib.call("lz_router_wgrad", ptr(dlogits), ptr(x), Tn, d, E, ptr(dwg), ptr(db), ptr(ws),
+              nbytes, _s())
+    return dwg, db
+
+
+def grouped_gemm_rows(A, B, off, C, *, b_major=_lib.LZ_K_MAJOR, epilogue=_lib.LZ_EPI_STORE,
+                      aux=None, num_sms: int = 0):
+    """C[off[g]:off[g+1]] = A[off[g]:off[g+1]] . B_g (+ fused epilogue).
+    A [rows, K]; B [G, N, K] (K-major) or [G, K, N] (MN-major); C [rows, N]."""
+    _cuda(A, B, off, C, aux)
+    rows, K = A.shape
+    G = off.numel() - 1
+    N = B.shape[1] if b_major == _lib.LZ_K_MAJOR else B.shape[2]
+    _lib.call("lz_grouped_gemm", 0, ptr(A), ptr(B), ptr(C), ptr(aux), G, ptr(off), rows, 0, N, K,
+              b_major, epilogue, num_sms, _s())
+    return C
+
+
+def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0):
+    """C[g] = A[off[g]:off[g+1]]^T . B[off[g]:off[g+1]]; A [rows, M], B [rows, N], C [G, M, N]."""
+    _cuda(A, B, off, C)
+    rows, M = A.shape
+    N = B.shape[1]
+    G = off.numel() - 1
+    _lib.call("lz_grouped_gemm", 1, ptr(A), ptr(B), ptr(C), None, G, ptr(off), rows, M, N, 0,
+              _lib.LZ_MN_MAJOR, _lib.LZ_EPI_STORE, num_sms, _s())
+    return C

@@ -1,0 +1,225 @@
+"""Generate golden vectors by running the REFERENCE itself (flexep, read-only at
+/root/reference/pkg/src).  Run in the build container only:
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/dispatch_golden.json and tests/golden/placement_golden.json.
+The fuzz instance generators below reproduce the input distributions of the
+reference's own tests (test_dispatch.py:164-174 seed 0xFA57 / 0x10CA1,
+test_acceptance.py:246-257 seed 0xD15B, test_dispatch.py:71-82 seed 0x0D15) so
+the oracle and the GPU planner are pinned on exactly the instances the
+reference pins itself on.  Large instance sets are stored as a sha256 digest of
+the canonical JSON of all outputs plus the first few outputs verbatim.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import random
+import sys
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def digest(obj) -> str:
+    return hashlib.sha256(json.dumps(obj, sort_keys=True, separators=(",", ":")).encode()).hexdigest()
+
+
+def gen_fuzz(rng, tmax):
+    """(T, R) instance as in test_dispatch.py:164-174 / test_acceptance.py:246-257."""
+    n = rng.randint(1, 6)
+    e = rng.randint(1, 6)
+    t = [[rng.randint(0, tmax) for _ in range(n)] for _ in range(e)]
+    rows = []
+    for _ in t:
+        owners = [rng.choice([0, 0, 1, 2, 3]) for _ in range(n)]
+        if sum(owners) == 0:
+            owners[rng.randrange(n)] = 1
+        rows.append(owners)
+    return t, rows
+
+
+def gen_owner_only(rng):
+    """(T, R) instance as in test_dispatch.py:71-82 (seed 0x0D15)."""
+    n = rng.randint(1, 5)
+    e = rng.randint(1, 5)
+    t = [[rng.randint(0, 30) for _ in range(n)] for _ in range(e)]
+    rows = []
+    for row in t:
+        owners = [rng.randint(0, 2) for _ in range(n)]
+        if sum(row) > 0 and sum(owners) == 0:
+            owners[rng.randrange(n)] = 1
+        rows.append(owners)
+    return t, rows
+
+
+def main() -> None:
+    sys.path.insert(0, REF)
+    from flexep.allocation import allocate_replicas, allocation_from_replicas
+    from flexep.core import ClusterSpec, split_evenly, split_proportionally
+    from flexep.dispatch import (ReplicaMatrix, UnroutableTokenError, build_shuffle_index,
+                                 compute_dispatch_schedule, full_dispatch_matrices,
+                                 simulate_all_to_all)
+    from flexep.migration import greedy_node_mapping
+    from flexep.placement import build_mro_plan
+
+    out: dict = {"generator": "tests/golden/make_golden.py", "reference": "flexep 0.1.0"}
+
+    # --- split_proportionally: KATs (test_core.py:147-159) + fuzz ------------
+    rng = random.Random(0x5917)
+    splits = [[10, [1, 1]], [9, [5, 5]], [0, [0, 0]], [17, [3, 0, 9, 1]], [4, [0, 7, 0]],
+              [10, [1, 1, 1, 1]]]
+    for _ in range(400):
+        n = rng.randint(1, 8)
+        w = [rng.choice([0, rng.randint(0, 5), rng.randint(0, 1 << 20)]) for _ in range(n)]
+        if sum(w) == 0:
+            w[0] = 1
+        splits.append([rng.randint(0, 1 << 22), w])
+    out["split"] = [[t, w, split_proportionally(t, w)] for t, w in splits]
+    out["split_evenly"] = [[10, 4, split_evenly(10, 4)], [0, 2, split_evenly(0, 2)]]
+
+    # --- dispatch KATs (test_dispatch.py) ------------------------------------
+    kat = []
+    for t, r in ([[[5, 5]], [[1, 0]]], [[[4, 4], [4, 4]], [[1, 1], [1, 1]]],
+                 [[[0, 0, 9]], [[1, 1, 0]]], [[[0, 0]], [[0, 0]]],
+                 [[[3, 0], [2, 2]], [[1, 0], [0, 1]]], [[[2], [2]], [[1], [1]]],
+                 [[[4, 2, 1], [1, 3, 2]], [[1, 1, 0], [0, 1, 1]]]):
+        rm = ReplicaMatrix(tuple(tuple(x) for x in r))
+        kat.append({"T": t, "R": r,
+                    "schedules": [compute_dispatch_schedule(i, t, rm).to_dict()
+                                  for i in range(len(t[0]))]})
+    out["kat"] = kat
+    out["unroutable"] = {"T": [[3]], "R": [[0]]}
+    try:
+        compute_dispatch_schedule(0, [[3]], ReplicaMatrix(((0,),)))
+        raise SystemExit("reference did not raise")
+    except UnroutableTokenError:
+        pass
+
+    # shuffle KATs
+    t, r = [[3, 0], [2, 2]], ((1, 0), (0, 1))
+    s0 = compute_dispatch_schedule(0, t, ReplicaMatrix(r))
+    s = compute_dispatch_schedule(0, [[2], [2]], ReplicaMatrix(((1,), (1,))))
+    out["shuffle_kat"] = [
+        {"D": [list(x) for x in s0.send_counts], "routed": [0, 1, 0, 1, 0],
+         "index": build_shuffle_index(s0, [0, 1, 0, 1, 0])},
+        {"D": [list(x) for x in s.send_counts], "routed": [1, 0, 1, 0],
+         "index": build_shuffle_index(s, [1, 0, 1, 0])},
+    ]
+
+    # c12 (test_acceptance.py:581-617) dispatch part
+    spec = ClusterSpec(n_nodes=6, slots_per_node=4, fault_threshold=2)
+    alloc = allocate_replicas([5, 9, 14, 2, 31, 8], spec)
+    plan = build_mro_plan(alloc, spec)
+    rm = ReplicaMatrix.from_plan(plan)
+    tt = [[3, 1, 4, 1, 5, 9] for _ in range(6)]
+    out["c12"] = {"loads": [5, 9, 14, 2, 31, 8], "n": 6, "c": 4, "f": 2,
+                  "replicas": list(alloc.replicas), "R": [list(x) for x in rm.counts], "T": tt,
+                  "schedules": [compute_dispatch_schedule(i, tt, rm).to_dict() for i in range(6)]}
+
+    # --- fuzz sets, digested ---------------------------------------------------
+    def run_set(seed, count, tmax, gen="fuzz"):
+        rng = random.Random(seed)
+        results = []
+        for _ in range(count):
+            t, r = gen_fuzz(rng, tmax) if gen == "fuzz" else gen_owner_only(rng)
+            rm = ReplicaMatrix(tuple(tuple(x) for x in r))
+            try:
+                mats = full_dispatch_matrices(t, rm)
+                scheds = [compute_dispatch_schedule(i, t, rm).to_dict() for i in range(len(t[0]))]
+                simulate_all_to_all([compute_dispatch_schedule(i, t, rm) for i in range(len(t[0]))])
+                results.append({"T": t, "R": r, "D": mats, "schedules": scheds})
+            except UnroutableTokenError:
+                results.append({"T": t, "R": r, "error": "unroutable"})
+        return results
+
+    sets = {}
+    for name, seed, count, tmax, gen in (("c07", 0xD15B, 10000, 50, "fuzz"),
+                                         ("fa57", 0xFA57, 500, 40, "fuzz"),
+                                         ("loca1", 0x10CA1, 300, 40, "fuzz"),
+                                         ("d15", 0x0D15, 200, 30, "owner")):
+        res = run_set(seed, count, tmax, gen)
+        sets[name] = {"seed": seed, "count": count, "tmax": tmax, "gen": gen,
+                      "digest": digest(res), "head": res[:40]}
+    out["fuzz"] = sets
+
+    # --- shuffle index on random routings --------------------------------------
+    rng = random.Random(0x5AFF)
+    shuf = []
+    for _ in range(150):
+        t, r = gen_fuzz(rng, 40)
+        rm = ReplicaMatrix(tuple(tuple(x) for x in r))
+        n_r = len(t[0])
+        rank = rng.randrange(n_r)
+        sch = compute_dispatch_schedule(rank, t, rm)
+        routed = [e for e in range(len(t)) for _ in range(t[e][rank])]
+        rng.shuffle(routed)
+        shuf.append({"T": t, "R": r, "rank": rank, "routed": routed,
+                     "index": build_shuffle_index(sch, routed)})
+    out["shuffle"] = shuf
+
+    with open(os.path.join(HERE, "dispatch_golden.json"), "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+
+    # --- placement plans (host-side plan producer) -----------------------------
+    pl = {"generator": "tests/golden/make_golden.py"}
+    cases = []
+    rng = random.Random(0x91A7)
+    fixed = [([5, 9, 14, 2, 31, 8], 6, 4, 2), ([25, 25, 25, 25], 5, 4, 2), ([10, 10, 10, 70], 5, 4, 2),
+             ([1, 1, 1, 97], 5, 4, 2), ([0, 0, 0, 0], 2, 2, 2)]
+    for _ in range(300):
+        E = rng.randint(1, 64)
+        n = rng.randint(1, 8)
+        c = rng.randint(max(1, -(-E // n)), max(1, -(-E // n)) + 6)
+        f = rng.randint(0, min(3, n))
+        s = rng.choice([0.0, 0.8, 1.2, 2.5])
+        perm = list(range(E))
+        rng.shuffle(perm)
+        loads = [int(1e5 * (1 + perm[e]) ** (-s)) + rng.randint(0, 50) for e in range(E)]
+        fixed.append((loads, n, c, f))
+    for loads, n, c, f in fixed:
+        spec = ClusterSpec(n_nodes=n, slots_per_node=c, fault_threshold=f)
+        alloc = allocate_replicas(loads, spec)
+        plan = build_mro_plan(alloc, spec)
+        cases.append({"loads": loads, "n": n, "c": c, "f": f,
+                      "replicas": list(alloc.replicas), "sorted_order": list(alloc.sorted_order),
+                      "f_used": alloc.f_used, "slots": [list(x) for x in plan.slots],
+                      "R": [list(x) for x in ReplicaMatrix.from_plan(plan).counts]})
+    pl["plans"] = cases
+    pl["from_plan_kat"] = {"replicas": [2, 4], "n": 3, "c": 2,
+                           "R": [list(x) for x in ReplicaMatrix.from_plan(build_mro_plan(
+                               allocation_from_replicas((2, 4)),
+                               ClusterSpec(n_nodes=3, slots_per_node=2))).counts]}
+    # greedy node mapping for elastic re-plans 8 -> 6 -> 4
+    maps = []
+    rng = random.Random(0x6EED)
+    for _ in range(60):
+        E = rng.choice([8, 16, 64])
+        n_old = 8
+        c = rng.choice([-(-E // 4), -(-3 * E // 8), -(-E // 2)])
+        loads = [rng.randint(1, 1000) for _ in range(E)]
+        spec = ClusterSpec(n_nodes=n_old, slots_per_node=c, fault_threshold=2)
+        old = build_mro_plan(allocate_replicas(loads, spec), spec)
+        live = sorted(rng.sample(range(n_old), rng.randint(2, 7)))
+        holdings = {node: set(old.col_sets[node]) for node in live}
+        spec2 = ClusterSpec(n_nodes=len(live), slots_per_node=c, fault_threshold=min(2, len(live)))
+        try:
+            new = build_mro_plan(allocate_replicas(loads, spec2), spec2)
+        except Exception:  # infeasible shrink -- skip
+            continue
+        cols = [set(new.col_sets[j]) for j in range(len(live))]
+        m = greedy_node_mapping(holdings, cols, live)
+        maps.append({"E": E, "c": c, "loads": loads, "old_slots": [list(x) for x in old.slots],
+                     "live": live, "new_slots": [list(x) for x in new.slots],
+                     "assignment": [list(a) for a in m.assignment]})
+    pl["node_mapping"] = maps
+    with open(os.path.join(HERE, "placement_golden.json"), "w") as f:
+        json.dump(pl, f, separators=(",", ":"))
+    print("wrote golden vectors")
+
+
+if __name__ == "__main__":
+    main()

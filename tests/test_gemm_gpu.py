@@ -1,0 +1,118 @@
+"""tcgen05 grouped GEMM (K4-K6) vs a torch fp32 reference of the same op.
+
+Tolerance: inputs are bf16, accumulation fp32, output rounded to bf16, so the
+error bound is ~2^-8 relative per element plus accumulation-order noise:
+|got - ref| <= 1e-2 * max|ref| + 1e-2 * |ref| elementwise.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2407_04656_b200 import _lib, ops  # noqa: E402
+
+
+def _close(got, ref, rtol=1e-2, atol_scale=1e-2):
+    got = got.float()
+    ref = ref.float()
+    tol = atol_scale * ref.abs().max().clamp_min(1e-6) + rtol * ref.abs()
+    bad = (got - ref).abs() > tol
+    assert not bad.any(), f"{int(bad.sum())} / {bad.numel()} mismatches, max err " \
+                          f"{(got - ref).abs().max().item():.4g}, max ref {ref.abs().max().item():.4g}"
+
+
+def _offsets(sizes):
+    off = [0]
+    for s in sizes:
+        off.append(off[-1] + s)
+    return torch.tensor(off, dtype=torch.int32, device="cuda"), off
+
+
+@pytest.mark.parametrize("sizes,K,N", [([128], 64, 256), ([128, 256, 0, 384], 128, 256),
+                                       ([512, 128], 1024, 512), ([1024], 1024, 4096)])
+def test_rows_kmajor(sizes, K, N):
+    torch.manual_seed(0)
+    off_t, off = _offsets(sizes)
+    rows, G = off[-1], len(sizes)
+    A = torch.randn(rows, K, device="cuda").bfloat16()
+    B = (torch.randn(G, N, K, device="cuda") / K ** 0.5).bfloat16()
+    C = torch.full((rows, N), float("nan"), device="cuda").bfloat16()
+    ops.grouped_gemm_rows(A, B, off_t, C)
+    torch.cuda.synchronize()
+    for g in range(G):
+        a = A[off[g]:off[g + 1]].float()
+        _close(C[off[g]:off[g + 1]], a @ B[g].float().t())
+
+
+@pytest.mark.parametrize("sizes,K,N", [([128, 256], 128, 256), ([384, 0, 128], 512, 512)])
+def test_rows_mnmajor_b(sizes, K, N):
+    torch.manual_seed(1)
+    off_t, off = _offsets(sizes)
+    rows, G = off[-1], len(sizes)
+    A = torch.randn(rows, K, device="cuda").bfloat16()
+    B = (torch.randn(G, K, N, device="cuda") / K ** 0.5).bfloat16()  # [K, N] per group
+    C = torch.empty((rows, N), device="cuda").bfloat16()
+    ops.grouped_gemm_rows(A, B, off_t, C, b_major=_lib.LZ_MN_MAJOR)
+    torch.cuda.synchronize()
+    for g in range(G):
+        _close(C[off[g]:off[g + 1]], A[off[g]:off[g + 1]].float() @ B[g].float())
+
+
+def test_gelu_and_dgelu_epilogues():
+    torch.manual_seed(2)
+    sizes, K, N = [256, 128], 256, 512
+    off_t, off = _offsets(sizes)
+    rows, G = off[-1], len(sizes)
+    A = torch.randn(rows, K, device="cuda").bfloat16()
+    B = (torch.randn(G, N, K, device="cuda") / K ** 0.5).bfloat16()
+    H = torch.empty((rows, N), device="cuda").bfloat16()
+    Act = torch.empty((rows, N), device="cuda").bfloat16()
+    ops.grouped_gemm_rows(A, B, off_t, Act, epilogue=_lib.LZ_EPI_GELU, aux=H)
+    # dgelu: C = (A . B2) * gelu'(H)
+    B2 = (torch.randn(G, K, N, device="cuda") / K ** 0.5).bfloat16()
+    dH = torch.empty((rows, N), device="cuda").bfloat16()
+    ops.grouped_gemm_rows(A, B2, off_t, dH, b_major=_lib.LZ_MN_MAJOR,
+                          epilogue=_lib.LZ_EPI_DGELU, aux=H)
+    torch.cuda.synchronize()
+    for g in range(G):
+        sl = slice(off[g], off[g + 1])
+        pre = A[sl].float() @ B[g].float().t()
+        _close(H[sl], pre)
+        _close(Act[sl], torch.nn.functional.gelu(H[sl].float(), approximate="tanh"), rtol=2e-2)
+        h = H[sl].float().requires_grad_(True)
+        torch.nn.functional.gelu(h, approximate="tanh").backward(torch.ones_like(h))
+        _close(dH[sl], (A[sl].float() @ B2[g].float()) * h.grad, rtol=2e-2)
+
+
+@pytest.mark.parametrize("sizes,M,N", [([128], 128, 256), ([64, 0, 192, 128], 256, 512),
+                                       ([1024, 512], 1024, 256)])
+def test_wgrad_variable_k(sizes, M, N):
+    torch.manual_seed(3)
+    off_t, off = _offsets(sizes)
+    rows, G = off[-1], len(sizes)
+    A = torch.randn(rows, M, device="cuda").bfloat16()
+    B = torch.randn(rows, N, device="cuda").bfloat16()
+    C = torch.full((G, M, N), float("nan"), device="cuda").bfloat16()
+    ops.grouped_gemm_wgrad(A, B, off_t, C)
+    torch.cuda.synchronize()
+    for g in range(G):
+        sl = slice(off[g], off[g + 1])
+        ref = A[sl].float().t() @ B[sl].float()
+        if off[g + 1] == off[g]:
+            assert (C[g] == 0).all()
+        else:
+            _close(C[g], ref)
+
+
+def test_persistent_grid_smaller_than_tiles():
+    torch.manual_seed(4)
+    off_t, off = _offsets([640, 384])
+    K, N = 192, 768
+    A = torch.randn(off[-1], K, device="cuda").bfloat16()
+    B = (torch.randn(2, N, K, device="cuda") / K ** 0.5).bfloat16()
+    C = torch.empty((off[-1], N), device="cuda").bfloat16()
+    ops.grouped_gemm_rows(A, B, off_t, C, num_sms=3)  # 3 CTAs loop over 24 tiles
+    torch.cuda.synchronize()
+    for g in range(2):
+        _close(C[off[g]:off[g + 1]], A[off[g]:off[g + 1]].float() @ B[g].float().t())

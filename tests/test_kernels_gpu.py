@@ -1,0 +1,144 @@
+"""K1/K3/K7/K8 kernels vs the CPU oracle / torch fp32 references of the same op.
+
+Tolerances (written per check): routed expert ids are exact for identical fp32
+logits; fp32 softmax/weights 1e-5 abs; bf16 data movement is exact (pack) or one
+bf16 rounding of an fp32 result (combine, backward): |err| <= 8e-3 * |ref| + 1e-3 * max|ref|.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import moe_ref  # noqa: E402
+from paper_2407_04656_b200 import ops  # noqa: E402
+
+
+def _close(got, ref, rtol=8e-3, atol_scale=1e-3):
+    got, ref = got.float().cpu(), ref.float().cpu()
+    tol = atol_scale * ref.abs().max().clamp_min(1e-6) + rtol * ref.abs()
+    err = (got - ref).abs()
+    assert (err <= tol).all(), f"max err {err.max().item():.4g} (ref max {ref.abs().max().item():.4g})"
+
+
+@pytest.mark.parametrize("Tn,E,k,renorm", [(1000, 16, 2, False), (4096, 8, 2, True),
+                                           (333, 64, 1, False), (64, 5, 3, True)])
+def test_gate_topk_exact_ids(Tn, E, k, renorm):
+    g = torch.Generator().manual_seed(Tn + E)
+    logits = torch.randn(Tn, E, generator=g)
+    logits[::7, 1] = logits[::7, 0]  # exact ties -> lower id must win
+    idx, w, probs, hist = ops.gate_topk(logits.cuda(), k, renorm)
+    ridx, rw, rprobs = moe_ref.gate_ref(logits, k, renorm)
+    assert torch.equal(idx.cpu(), ridx)
+    assert torch.allclose(w.cpu(), rw, atol=1e-5)
+    assert torch.allclose(probs.cpu(), rprobs, atol=1e-5)
+    assert torch.equal(hist.cpu(), torch.bincount(ridx.reshape(-1).long(), minlength=E).int())
+
+
+@pytest.mark.parametrize("Tn,d,E,k", [(4096, 1024, 16, 2), (1000, 512, 8, 2), (257, 2048, 64, 1),
+                                      (100, 4096, 8, 2)])
+def test_router_gate(Tn, d, E, k):
+    g = torch.Generator().manual_seed(d)
+    x = torch.randn(Tn, d, generator=g).bfloat16()
+    wg = (torch.randn(E, d, generator=g) * 0.02).bfloat16()
+    bias = torch.randn(E, generator=g) * 0.5
+    idx, w, probs, hist = ops.router_gate(x.cuda(), wg.cuda(), bias.cuda(), k)
+    logits = x.float() @ wg.float().t() + bias
+    ridx, rw, rprobs = moe_ref.gate_ref(logits, k)
+    # fp32 accumulate in a different order: probabilities within 1e-4; ids equal except
+    # where the k-th / (k+1)-th logit margin is below 1e-3
+    assert torch.allclose(probs.cpu(), rprobs, atol=1e-4)
+    srt = logits.sort(dim=1, descending=True).values
+    margin = (srt[:, :k] - srt[:, 1:k + 1]).abs().min(dim=1).values
+    safe = margin > 1e-3
+    assert safe.float().mean() > 0.9
+    assert torch.equal(idx.cpu()[safe], ridx[safe])
+    assert int(hist.sum()) == Tn * k
+
+
+def _rows(Tn, k, n_rows, gen):
+    return torch.randperm(n_rows, generator=gen)[:Tn * k].int()
+
+
+def test_pack_exact_and_pad_zero():
+    gen = torch.Generator().manual_seed(5)
+    Tn, d, k = 3000, 1024, 2
+    x = torch.randn(Tn, d, generator=gen).bfloat16()
+    # expert-major padded layout: 3 experts with m = 2500, 0, 3500 (pads 60, 0, 84)
+    m = torch.tensor([2500, 0, 3500], dtype=torch.int32)
+    off = torch.tensor([0, 2560, 2560, 6144], dtype=torch.int32)
+    perm = torch.randperm(6000, generator=gen)
+    real_rows = torch.cat([torch.arange(0, 2500), torch.arange(2560, 2560 + 3500)])
+    row = real_rows[perm].int()
+    out = torch.full((6144, d), 7.0).bfloat16().cuda()
+    ops.pack(x.cuda(), row.cuda(), k, out, m.cuda(), off.cuda())
+    ref = torch.zeros(6144, d).bfloat16()
+    ref[row.long()] = x.repeat_interleave(k, dim=0)
+    assert torch.equal(out.cpu(), ref)
+
+
+def test_combine_and_backward():
+    gen = torch.Generator().manual_seed(6)
+    Tn, d, k, E = 2048, 1024, 2, 16
+    n_rows = Tn * k + 512
+    y = torch.randn(n_rows, d, generator=gen).bfloat16()
+    row = _rows(Tn, k, n_rows, gen)
+    w = torch.rand(Tn, k, generator=gen)
+    out = ops.combine(y.cuda(), row.cuda(), w.cuda(), k)
+    yr = y.float()[row.long()].view(Tn, k, d)
+    ref = (yr * w.unsqueeze(-1)).sum(1)
+    _close(out, ref)
+    # backward: dy rows and dw
+    dout = torch.randn(Tn, d, generator=gen).bfloat16()
+    dy = torch.full((n_rows, d), 3.0).bfloat16().cuda()
+    dw = ops.combine_bwd(dout.cuda(), y.cuda(), row.cuda(), w.cuda(), k, dy)
+    ref_dy = (dout.float().unsqueeze(1) * w.unsqueeze(-1)).reshape(Tn * k, d)
+    _close(dy.cpu()[row.long()], ref_dy)
+    ref_dw = (dout.float().unsqueeze(1) * yr).sum(-1)
+    _close(dw, ref_dw, rtol=1e-4, atol_scale=1e-4)
+    del E
+
+
+@pytest.mark.parametrize("renorm", [False, True])
+def test_dispatch_bwd_and_router_grads(renorm):
+    """dx = sum_s dxe[row] + dlogits . wg and dlogits from the softmax/top-k backward,
+    against torch autograd on the same fp32 math."""
+    gen = torch.Generator().manual_seed(7)
+    Tn, d, E, k = 1024, 512, 16, 2
+    x = torch.randn(Tn, d, generator=gen).bfloat16()
+    wg = (torch.randn(E, d, generator=gen) * 0.05).bfloat16()
+    logits = (x.float() @ wg.float().t()).requires_grad_(True)
+    idx, _, _ = moe_ref.gate_ref(logits, k, renorm)
+    probs = torch.softmax(logits, 1)
+    wsel = torch.gather(probs, 1, idx.long())
+    if renorm:
+        wsel = wsel / wsel.sum(1, keepdim=True)
+    dw = torch.randn(Tn, k, generator=gen)
+    (wsel * dw).sum().backward()
+    ref_dlog = logits.grad
+    n_rows = Tn * k
+    row = _rows(Tn, k, n_rows, gen)
+    dxe = torch.randn(n_rows, d, generator=gen).bfloat16()
+    dx, dlog = ops.dispatch_bwd(dxe.cuda(), row.cuda(), probs.detach().cuda(), idx.cuda(),
+                                dw.cuda(), wg.cuda(), renorm, Tn)
+    _close(dlog, ref_dlog, rtol=1e-4, atol_scale=1e-5)
+    ref_dx = dxe.float()[row.long()].view(Tn, k, d).sum(1) + ref_dlog @ wg.float()
+    _close(dx, ref_dx)
+    dwg, db = ops.router_wgrad(dlog, x.cuda())
+    _close(dwg, dlog.cpu().t() @ x.float(), rtol=1e-4, atol_scale=1e-4)
+    _close(db, dlog.cpu().sum(0), rtol=1e-4, atol_scale=1e-4)
+
+
+def test_copy_segments():
+    gen = torch.Generator().manual_seed(8)
+    d = 256
+    src = torch.randn(1000, d, generator=gen).bfloat16().cuda()
+    dst = torch.zeros(1200, d).bfloat16().cuda()
+    s = torch.tensor([0, 100, 600], dtype=torch.int32)
+    t = torch.tensor([500, 0, 900], dtype=torch.int32)
+    c = torch.tensor([100, 500, 250], dtype=torch.int32)
+    ops.copy_segments(src, dst, s.cuda(), t.cuda(), c.cuda(), 500)
+    for a, b, n in zip(s.tolist(), t.tolist(), c.tolist()):
+        assert torch.equal(dst[b:b + n].cpu(), src[a:a + n].cpu())
+    assert np.count_nonzero(dst[850:900].float().cpu().numpy()) == 0
