@@ -79,9 +79,19 @@ def exported_symbols() -> list[str]:
     return list(_SIGS)
 
 
+# kernels each entry point launches (for the bench's gpu_launches count)
+_KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
+            "lz_gate_topk": 1, "lz_router_gate": 1, "lz_invert_permutation": 1, "lz_pack": 1,
+            "lz_copy_segments": 1, "lz_combine": 1, "lz_combine_bwd": 1, "lz_dispatch_bwd": 1,
+            "lz_router_wgrad": 2, "lz_grouped_gemm": 1}
+launch_count = 0
+
+
 def call(name: str, *args) -> None:
+    global launch_count
     h = load()
     st = getattr(h, name)(*args)
+    launch_count += _KERNELS.get(name, 0)
     if st != LZ_OK:
         msg = h.lz_status_string(st).decode()
         if st == LZ_ERR_CUDA:

@@ -1,0 +1,94 @@
+"""Collective plumbing of the multi-GPU MoE layer (torch.distributed over NCCL).
+
+    load all-gather    gather_load_matrix (dispatch.py:95-107) as one all-gather of
+                       the E-int histograms K1 produces
+    a2a-v              the padding-free flexible all-to-all (SPEC.md:372-380,
+                       simulate_all_to_all dispatch.py:247-283 is its reference check)
+    replica-group AR   expert gradients summed over the expert's owner ranks
+                       {j : R[e][j] > 0}, one sub-communicator per
+                       distinct owner set, cached per plan version
+
+All functions work on any backend torch.distributed supports (NCCL on the B200
+box, gloo in the CPU tests of the host logic).
+"""
+
+from __future__ import annotations
+
+from typing import Sequence
+
+import torch
+import torch.distributed as dist
+
+
+def world(group=None) -> tuple[int, int]:
+    if not dist.is_available() or not dist.is_initialized():
+        return 0, 1
+    return dist.get_rank(group), dist.get_world_size(group)
+
+
+def allgather_hist(hist: torch.Tensor, group=None) -> torch.Tensor:
+    """Per-rank expert histograms (int32 [E]) -> load matrix T [E, N] (int32)."""
+    rank, n = world(group)
+    if n == 1:
+        return hist.view(-1, 1).contiguous()
+    out = torch.empty(n * hist.numel(), dtype=hist.dtype, device=hist.device)
+    dist.all_gather_into_tensor(out, hist.contiguous(), group=group)
+    return out.view(n, -1).t().contiguous()
+
+
+def all_to_all_rows(out: torch.Tensor, inp: torch.Tensor, out_splits: Sequence[int],
+                    in_splits: Sequence[int], group=None) -> torch.Tensor:
+    """Row all-to-all-v: rank i sends in_splits[j] rows to rank j and receives
+    out_splits[j] rows from rank j (no padding)."""
+    dist.all_to_all_single(out, inp, [int(v) for v in out_splits], [int(v) for v in in_splits],
+                           group=group)
+    return out
+
+
+def owner_sets(R: Sequence[Sequence[int]]) -> list[tuple[int, ...]]:
+    """owners[e] = ranks hosting at least one replica of expert e."""
+    return [tuple(j for j, v in enumerate(row) if v > 0) for row in R]
+
+
+class ReplicaGroups:
+    """Sub-communicators for the replica-group gradient all-reduce.
+
+    Built collectively (every rank creates every group, in the same sorted order,
+    as torch.distributed requires) once per plan; experts sharing an owner set share
+    a communicator and their gradients travel in one bucket."""
+
+    def __init__(self, R: Sequence[Sequence[int]], group=None, backend: str | None = None):
+        self.rank, self.n = world(group)
+        self.owners = owner_sets(R)
+        self.sets = sorted({o for o in self.owners if len(o) > 1})
+        self.groups: dict[tuple[int, ...], object] = {}
+        if self.n > 1:
+            base = dist.get_process_group_ranks(group) if group is not None else list(range(self.n))
+            for s in self.sets:
+                pg = dist.new_group([base[j] for j in s], backend=backend)
+                if self.rank in s:
+                    self.groups[s] = pg
+
+    def buckets(self, local_ids: Sequence[int]) -> list[tuple[object, list[int]]]:
+        """[(process group, local expert positions)] for this rank."""
+        out: dict[tuple[int, ...], list[int]] = {}
+        for pos, e in enumerate(local_ids):
+            s = self.owners[e]
+            if len(s) > 1:
+                out.setdefault(s, []).append(pos)
+        return [(self.groups[s], pos) for s, pos in sorted(out.items())]
+
+    def allreduce(self, grads: Sequence[torch.Tensor], local_ids: Sequence[int]) -> None:
+        """Sum each local expert's gradient slices ([E_loc, ...] tensors) over the
+        expert's owner ranks, in place."""
+        if self.n == 1:
+            return
+        for pg, pos in self.buckets(local_ids):
+            idx = torch.tensor(pos, device=grads[0].device)
+            flat = torch.cat([g.index_select(0, idx).reshape(-1) for g in grads])
+            dist.all_reduce(flat, group=pg)
+            o = 0
+            for g in grads:
+                n = g[0].numel() * len(pos)
+                g.index_copy_(0, idx, flat[o:o + n].view(len(pos), *g.shape[1:]))
+                o += n

@@ -1,0 +1,282 @@
+"""MoELayer: the Lazarus MoE-layer hot path on B200 (fwd + bwd + replica-group sync).
+
+Per rank, per step:
+    K1 router_gate      x . wg^T + b -> softmax / top-k -> idx, w, probs, hist
+    all-gather hist     -> T [E, N]                                   (N > 1)
+    K2 plan_device      bit-exact reference dispatch: D, sizes, slot, dest_row
+    K3 pack             rows -> expert-major padded receive buffer (N = 1 directly;
+                        N > 1 via send buffer -> NCCL a2a-v -> segment regroup)
+    K4 grouped GEMM x2  X W1^T (+GELU epilogue, keeps pre-activation), A W2^T
+    K7 combine          (N > 1 after the reverse a2a-v) weighted sum of the k outputs
+backward:
+    K8 combine_bwd -> [a2a] -> K5 dgrad (dY W2 . gelu'(H), dH W1) + K6 wgrad
+    (variable-K, per expert) -> [a2a] -> K8 dispatch/gate bwd -> router wgrad
+    -> replica-group all-reduce of expert grads, DP all-reduce of router grads.
+
+One weight copy per (expert, rank) hosting it: R[e][rank] > 1 only
+raises the capacity the planner gives that rank.  At N = 1 the whole step is free
+of host synchronisation (CUDA-graph capturable); device-side plan errors are then
+surfaced by :meth:`MoELayer.check`.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _lib, comm, ops
+from .dispatch import DevicePlan, ReplicaMatrix, plan_device
+
+ALIGN = ops.ALIGN
+
+
+def _expert_weights(seed: int, e: int, shape, std: float, device) -> torch.Tensor:
+    """Deterministic per-expert init: every owner rank of expert e builds the same copy."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed * 1_000_003 + e)
+    return (torch.randn(shape, generator=g, device=device) * std).to(torch.bfloat16)
+
+
+class MoELayer(torch.nn.Module):
+    def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int = 2, *,
+                 replicas=None, group=None, renorm: bool = False, seed: int = 0,
+                 init_std: float = 0.02, router_bias=None, device=None):
+        super().__init__()
+        if d_model % 256 or d_ff % 256:
+            raise ValueError("d_model and d_ff must be multiples of 256 (GEMM tile)")
+        if not 1 <= top_k <= min(n_experts, _lib.LZ_MAX_TOPK) or n_experts > 64:
+            raise ValueError("need 1 <= top_k <= min(E, 8) and E <= 64")
+        self.d, self.d_ff, self.E, self.k = d_model, d_ff, n_experts, top_k
+        self.renorm = renorm
+        self.group = group
+        self.seed = seed
+        self.init_std = init_std
+        self.rank, self.world = comm.world(group)
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.device = dev
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.wg = torch.nn.Parameter(
+            (torch.randn(n_experts, d_model, generator=g, device=dev) * init_std).bfloat16())
+        bias = torch.zeros(n_experts, device=dev) if router_bias is None else \
+            torch.as_tensor(router_bias, dtype=torch.float32, device=dev)
+        self.bg = torch.nn.Parameter(bias.float().clone())
+        self.w1 = None
+        self.w2 = None
+        self.last_plan: DevicePlan | None = None
+        self.set_plan(replicas)
+
+    # ------------------------------------------------------------- plan
+    def set_plan(self, replicas, weights: dict | None = None) -> None:
+        """Install a (new) replica matrix in communicator-rank order.  Experts this rank
+        keeps retain their weights; newly hosted experts take ``weights[e] = (w1, w2)``
+        (state migrated from a surviving owner) or the deterministic init.  No kernel is
+        recompiled: E and N are runtime arguments of every kernel."""
+        if replicas is None:
+            R = [[1] * self.world for _ in range(self.E)]
+        elif isinstance(replicas, ReplicaMatrix):
+            R = [list(r) for r in replicas.counts]
+        else:
+            R = [list(r) for r in replicas]
+        if len(R) != self.E or any(len(r) != self.world for r in R):
+            raise ValueError(f"replica matrix must be {self.E} x {self.world}")
+        for e, row in enumerate(R):
+            if sum(row) == 0:
+                raise ValueError(f"expert {e} has no replica")
+        old = {}
+        if self.w1 is not None:
+            for pos, e in enumerate(self.local_ids):
+                old[e] = (self.w1.data[pos], self.w2.data[pos])
+        self.R = R
+        self.R_dev = torch.tensor(R, dtype=torch.int32, device=self.device)
+        self.local_ids = [e for e in range(self.E) if R[e][self.rank] > 0]
+        ext = self.local_ids + [self.E]
+        self._off_index = torch.tensor(ext, dtype=torch.long, device=self.device)
+        w1s, w2s = [], []
+        for e in self.local_ids:
+            if weights is not None and e in weights:
+                a, b = weights[e]
+            elif e in old:
+                a, b = old[e]
+            else:
+                a = _expert_weights(self.seed, 2 * e, (self.d_ff, self.d), self.init_std, self.device)
+                b = _expert_weights(self.seed, 2 * e + 1, (self.d, self.d_ff), self.init_std,
+                                    self.device)
+            w1s.append(a)
+            w2s.append(b)
+        # w1[g] = W1_e [d_ff, d], w2[g] = W2_e [d, d_ff] (row-major, K contiguous for fwd)
+        self.w1 = torch.nn.Parameter(torch.stack(w1s).contiguous())
+        self.w2 = torch.nn.Parameter(torch.stack(w2s).contiguous())
+        self.replica_groups = comm.ReplicaGroups(R, self.group) if self.world > 1 else None
+
+    def expert_state(self) -> dict:
+        return {e: (self.w1.data[p], self.w2.data[p]) for p, e in enumerate(self.local_ids)}
+
+    def check(self) -> None:
+        """Raise the reference's exception if the last plan flagged an error (syncs)."""
+        if self.last_plan is not None:
+            self.last_plan.check()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        return _MoEFunction.apply(x, self.wg, self.bg, self.w1, self.w2, self)
+
+    # ------------------------------------------------------------- stats
+    def imbalance(self) -> float:
+        """max_j recv_j / mean_j recv_j of the last plan."""
+        p = self.last_plan
+        if p is None:
+            return float("nan")
+        recv = p.D.sum(dim=(0, 1)).float()
+        return float(recv.max() / recv.mean().clamp_min(1))
+
+
+def _capacity(rows: int) -> int:
+    return (rows + ALIGN - 1) // ALIGN * ALIGN
+
+
+class _MoEFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, wg, bg, w1, w2, layer: MoELayer):
+        if not x.is_cuda or x.dtype != torch.bfloat16 or x.dim() != 2:
+            raise ValueError("x must be a CUDA bf16 [tokens, d_model] tensor")
+        x = x.contiguous()
+        Tn, d = x.shape
+        k, E, G = layer.k, layer.E, len(layer.local_ids)
+        N, rank, group = layer.world, layer.rank, layer.group
+        idx, w, probs, hist = ops.router_gate(x, wg, bg, k, layer.renorm)
+        T = comm.allgather_hist(hist, group)
+        plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ALIGN)
+        layer.last_plan = plan
+        off = plan.recv_off.index_select(0, layer._off_index).contiguous()
+        P = Tn * k
+        if N == 1:
+            cap = _capacity(P + E * (ALIGN - 1))
+            X = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
+            ops.pack(x, plan.dest_row, k, X, plan.recv_m, plan.recv_off)
+            sizes = None
+        else:
+            # v1 exchange: one D2H of the counts (+ error flag) per layer forward
+            host = torch.cat([plan.send_sizes, plan.recv_counts, plan.err,
+                              plan.recv_cnt.max().view(1)]).cpu()
+            err = int(host[2 * N])
+            if err:
+                plan.check()
+            send_sizes = host[:N].tolist()
+            recv_counts = host[N:2 * N].tolist()
+            max_seg = int(host[2 * N + 1])
+            sizes = (send_sizes, recv_counts, max_seg)
+            n_recv = sum(recv_counts)
+            cap = _capacity(n_recv + E * (ALIGN - 1))
+            send = torch.empty((P, d), dtype=torch.bfloat16, device=x.device)
+            ops.pack(x, plan.slot, k, send)
+            stage = torch.empty((n_recv, d), dtype=torch.bfloat16, device=x.device)
+            comm.all_to_all_rows(stage, send, recv_counts, send_sizes, group)
+            X = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
+            ops.zero_pad_rows(X, plan.recv_m, plan.recv_off)
+            ops.copy_segments(stage, X, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
+                              max_seg)
+            del send, stage
+        d_ff = layer.d_ff
+        H = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
+        A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
+        Y = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
+        if G > 0:
+            ops.grouped_gemm_rows(X, w1, off, A, epilogue=_lib.LZ_EPI_GELU, aux=H)
+            ops.grouped_gemm_rows(A, w2, off, Y)
+        if N == 1:
+            out = ops.combine(Y, plan.dest_row, w, k)
+            ret, row = Y, plan.dest_row
+        else:
+            send_sizes, recv_counts, max_seg = sizes
+            Yst = torch.empty((sum(recv_counts), d), dtype=torch.bfloat16, device=x.device)
+            ops.copy_segments(Y, Yst, plan.recv_src_off, plan.recv_stage_off, plan.recv_cnt,
+                              max_seg)
+            ret = torch.empty((P, d), dtype=torch.bfloat16, device=x.device)
+            comm.all_to_all_rows(ret, Yst, send_sizes, recv_counts, group)
+            out = ops.combine(ret, plan.slot, w, k)
+            row = plan.slot
+        ctx.layer = layer
+        ctx.meta = (Tn, cap, sizes)
+        ctx.plan = plan
+        ctx.save_for_backward(x, wg, w1, w2, idx, w, probs, off, X, H, A, ret, row)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        layer: MoELayer = ctx.layer
+        x, wg, w1, w2, idx, w, probs, off, X, H, A, ret, row = ctx.saved_tensors
+        plan: DevicePlan = ctx.plan
+        Tn, cap, sizes = ctx.meta
+        k, N, group = layer.k, layer.world, layer.group
+        d, d_ff = layer.d, layer.d_ff
+        G = len(layer.local_ids)
+        dout = dout.contiguous().to(torch.bfloat16)
+        dev = x.device
+        if N == 1:
+            dY = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
+            dw = ops.combine_bwd(dout, ret, row, w, k, dY, plan.recv_m, plan.recv_off)
+        else:
+            send_sizes, recv_counts, max_seg = sizes
+            dret = torch.empty_like(ret)
+            dw = ops.combine_bwd(dout, ret, row, w, k, dret)
+            stage = torch.empty((sum(recv_counts), d), dtype=torch.bfloat16, device=dev)
+            comm.all_to_all_rows(stage, dret, recv_counts, send_sizes, group)
+            dY = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
+            ops.zero_pad_rows(dY, plan.recv_m, plan.recv_off)
+            ops.copy_segments(stage, dY, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
+                              max_seg)
+            del dret, stage
+        dH = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=dev)
+        dX = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
+        dW1 = torch.empty_like(w1)
+        dW2 = torch.empty_like(w2)
+        if G > 0:
+            # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * gelu'(H)
+            ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR,
+                                  epilogue=_lib.LZ_EPI_DGELU, aux=H)
+            # dX = dH . W1 (W1_e [d_ff, d] read MN-major)
+            ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR)
+            # variable-K weight gradients: dW1_e = dH_e^T X_e, dW2_e = dY_e^T A_e
+            ops.grouped_gemm_wgrad(dH, X, off, dW1)
+            ops.grouped_gemm_wgrad(dY, A, off, dW2)
+        if N == 1:
+            dxe, drow = dX, row
+        else:
+            send_sizes, recv_counts, max_seg = sizes
+            dXst = torch.empty((sum(recv_counts), d), dtype=torch.bfloat16, device=dev)
+            ops.copy_segments(dX, dXst, plan.recv_src_off, plan.recv_stage_off, plan.recv_cnt,
+                              max_seg)
+            dxe = torch.empty((Tn * k, d), dtype=torch.bfloat16, device=dev)
+            comm.all_to_all_rows(dxe, dXst, send_sizes, recv_counts, group)
+            drow = row
+        dx, dlog = ops.dispatch_bwd(dxe, drow, probs, idx, dw, wg, layer.renorm, Tn)
+        dwg, dbg = ops.router_wgrad(dlog, x)
+        if N > 1:
+            layer.replica_groups.allreduce([dW1, dW2], layer.local_ids)
+            flat = torch.cat([dwg.view(-1), dbg])
+            dist.all_reduce(flat, group=group)
+            dwg = flat[:dwg.numel()].view_as(dwg)
+            dbg = flat[dwg.numel():]
+        return dx, dwg.to(wg.dtype), dbg, dW1, dW2, None
+
+
+def zipf_router_bias(n_experts: int, s: float, seed: int = 0) -> torch.Tensor:
+    """log p_e with p_e ~ (1 + pi(e))^-s for a seeded permutation pi: makes the learned
+    router's top-k a Zipf(s) sample (SURVEY.md 8d synthetic inputs)."""
+    g = torch.Generator().manual_seed(seed)
+    perm = torch.randperm(n_experts, generator=g).float()
+    p = (1.0 + perm) ** (-s)
+    p = p / p.sum()
+    return torch.log(p)
+
+
+def default_slots(n_experts: int, n_ranks: int, factor: int = 3) -> int:
+    """c = ceil(factor * E / N)."""
+    return math.ceil(factor * n_experts / n_ranks)
+
+
+__all__ = ["MoELayer", "zipf_router_bias", "default_slots"]
+_ = Sequence

@@ -123,6 +123,23 @@ def router_wgrad(dlogits, x, with_bias: bool = True):
     return dwg, db
 
 
+# Optional timing hook: when set to a list, every grouped-GEMM launch appends a
+# (start, end) pair of CUDA events recorded on the launching stream (bench.py).
+GEMM_EVENTS: list | None = None
+
+
+def _gemm(*args):
+    if GEMM_EVENTS is None:
+        _lib.call("lz_grouped_gemm", *args)
+        return
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
+    _lib.call("lz_grouped_gemm", *args)
+    b.record()
+    GEMM_EVENTS.append((a, b))
+
+
 def grouped_gemm_rows(A, B, off, C, *, b_major=_lib.LZ_K_MAJOR, epilogue=_lib.LZ_EPI_STORE,
                       aux=None, num_sms: int = 0):
     """C[off[g]:off[g+1]] = A[off[g]:off[g+1]] . B_g (+ fused epilogue).
@@ -131,8 +148,8 @@ def grouped_gemm_rows(A, B, off, C, *, b_major=_lib.LZ_K_MAJOR, epilogue=_lib.LZ
     rows, K = A.shape
     G = off.numel() - 1
     N = B.shape[1] if b_major == _lib.LZ_K_MAJOR else B.shape[2]
-    _lib.call("lz_grouped_gemm", 0, ptr(A), ptr(B), ptr(C), ptr(aux), G, ptr(off), rows, 0, N, K,
-              b_major, epilogue, num_sms, _s())
+    _gemm(0, ptr(A), ptr(B), ptr(C), ptr(aux), G, ptr(off), rows, 0, N, K, b_major, epilogue,
+          num_sms, _s())
     return C
 
 
@@ -142,6 +159,6 @@ def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0):
     rows, M = A.shape
     N = B.shape[1]
     G = off.numel() - 1
-    _lib.call("lz_grouped_gemm", 1, ptr(A), ptr(B), ptr(C), None, G, ptr(off), rows, M, N, 0,
-              _lib.LZ_MN_MAJOR, _lib.LZ_EPI_STORE, num_sms, _s())
+    _gemm(1, ptr(A), ptr(B), ptr(C), None, G, ptr(off), rows, M, N, 0, _lib.LZ_MN_MAJOR,
+          _lib.LZ_EPI_STORE, num_sms, _s())
     return C
