@@ -68,8 +68,13 @@ def test_layer_matches_oracle(Tn, d, dff, E, k, s, renorm):
     ref.backward(dout.float().cpu())
     _rel(out, ref, name="out")
     _rel(x.grad, xr.grad, name="dx")
-    _rel(layer.wg.grad, wg.grad, l2=5e-2, linf=1e-1, name="dwg")
-    _rel(layer.bg.grad, bg.grad, l2=5e-2, linf=1e-1, name="dbg")
+    if k == 1 and renorm:
+        # w = p / p = 1: the router receives no gradient (the oracle's is fp32 noise)
+        assert float(layer.wg.grad.float().abs().max()) < 1e-4
+        assert float(wg.grad.abs().max()) < 1e-4
+    else:
+        _rel(layer.wg.grad, wg.grad, l2=5e-2, linf=1e-1, name="dwg")
+        _rel(layer.bg.grad, bg.grad, l2=5e-2, linf=1e-1, name="dbg")
     for p, e in enumerate(layer.local_ids):
         _rel(layer.w1.grad[p], w1.grad[e], name=f"dW1[{e}]")
         _rel(layer.w2.grad[p], w2.grad[e], name=f"dW2[{e}]")
