@@ -26,8 +26,19 @@ constexpr int kBTileBytes = BN * BK * 2;  // 32 KB
 constexpr int kStageBytes = kATileBytes + kBTileBytes;
 constexpr int kAccCols = BN;              // fp32 accumulator columns per buffer
 constexpr int kTmemCols = 2 * kAccCols;   // 512
-constexpr int kMaxGroups = 1024;
-constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int kMaxGroups = 128;
+// epilogue staging: each epilogue warp owns 32 rows; chunks of 32 columns (64 B rows,
+// 64B-swizzled, 2 KB) double-buffered for the output and for the aux stream
+// (GELU pre-activation out / dGELU pre-activation in)
+constexpr int kEpiCols = 32;
+constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
+constexpr int kEpiWarpBytes = 4 * kEpiBuf;          // out0 out1 aux0 aux1
+constexpr int kEpiBytes = 4 * kEpiWarpBytes;        // 32 KB
+constexpr int kTilesBytes = kStages * kStageBytes;  // 192 KB
+constexpr int kBarBytes = 256;
+constexpr int kTabBytes = 2 * (kMaxGroups + 1) * 4;
+constexpr int kSmemBytes = 1024 /*align slack*/ + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
+static_assert(kSmemBytes <= 232448, "shared memory budget");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -71,6 +82,41 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
+                                             int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   map),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+// byte offset of 16-byte piece q of row r inside a 64B-swizzled [32 x 64 B] staging tile
+__device__ __forceinline__ int stg_off(int r, int q) { return r * 64 + ((q ^ ((r >> 1) & 3)) << 4); }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -146,8 +192,6 @@ struct Params {
   int G;            // groups
   int M, N, K;      // mode 0: N, K used; mode 1: M, N
   const int32_t* off;
-  __nv_bfloat16* C;
-  __nv_bfloat16* aux;
   int epilogue;
 };
 
@@ -200,21 +244,25 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
 template <int A_MN, int B_MN>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                        const __grid_constant__ CUtensorMap map_b, const Params p) {
+                        const __grid_constant__ CUtensorMap map_b,
+                        const __grid_constant__ CUtensorMap map_c,
+                        const __grid_constant__ CUtensorMap map_x, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* s_tiles = smem;
-  uint64_t* full_bar = (uint64_t*)(smem + kStages * kStageBytes);
+  uint8_t* s_epi = smem + kTilesBytes;
+  uint64_t* full_bar = (uint64_t*)(s_epi + kEpiBytes);
   uint64_t* empty_bar = full_bar + kStages;
   uint64_t* tfull_bar = empty_bar + kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* s_tmem = (uint32_t*)(tempty_bar + 2);
-  __shared__ int32_t s_off[kMaxGroups + 1];
-  __shared__ int32_t s_pref[kMaxGroups + 1];
+  uint64_t* aux_bar = tempty_bar + 2;  // [4 warps][2 buffers]
+  uint32_t* s_tmem = (uint32_t*)(aux_bar + 8);
+  int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
+  int32_t* s_pref = s_off + kMaxGroups + 1;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 
-  // group table -> tile prefix (every CTA computes it; G <= 1024)
+  // group table -> tile prefix (every CTA computes it; G <= kMaxGroups)
   for (int g = threadIdx.x; g <= p.G; g += blockDim.x) s_off[g] = p.off[g];
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -235,9 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], 128);
     }
+    for (int s = 0; s < 8; ++s) mbar_init(&aux_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
+    if (p.epilogue != LZ_EPI_STORE) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -322,66 +373,95 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===== epilogue warps 2..5 =====
+    // ===== epilogue warps 2..5: TMEM -> regs -> activation -> swizzled smem -> TMA store
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    const int r = quad * 32 + lane;
+    uint8_t* wbuf = s_epi + quad * kEpiWarpBytes;
+    const uint32_t out_s = smem_u32(wbuf);                 // out0, out1
+    const uint32_t aux_s = smem_u32(wbuf + 2 * kEpiBuf);   // aux0, aux1
+    uint64_t* my_aux_bar = aux_bar + quad * 2;
+    uint32_t aux_phase[2] = {0, 0};
+    const bool gelu = p.epilogue == LZ_EPI_GELU, dgelu = p.epilogue == LZ_EPI_DGELU;
+    constexpr int kChunks = BN / kEpiCols;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const TileInfo t = decode_tile(p, s_pref, s_off, tile);
-      long row;
-      __nv_bfloat16* cbase;
-      __nv_bfloat16* abase = nullptr;
-      if (p.mode == 0) {
-        row = (long)s_off[t.g] + t.mb * BM + r;
-        cbase = p.C + row * p.N + t.nb * BN;
-        if (p.aux) abase = p.aux + row * p.N + t.nb * BN;
-      } else {
-        row = (long)t.mb * BM + r;
-        cbase = p.C + (long)t.g * p.M * p.N + row * p.N + t.nb * BN;
+      const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.M) + t.mb * BM + quad * 32;
+      const int col0 = t.nb * BN;
+      if (dgelu && lane == 0) {
+        // prefetch the first two pre-activation chunks of this tile
+        fence_async_smem();
+        for (int c = 0; c < 2; ++c) {
+          mbar_expect_tx(&my_aux_bar[c], kEpiBuf);
+          tma_load_2d(wbuf + (2 + c) * kEpiBuf, &map_x, &my_aux_bar[c], col0 + c * kEpiCols, row0);
+        }
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < kChunks; ++c) {
+        const int b = c & 1;
         uint32_t v[32];
         if (t.nk > 0) {
-          tmem_ld32(taddr + c * 32, v);
+          tmem_ld32(taddr + c * kEpiCols, v);
         } else {
 #pragma unroll
           for (int q = 0; q < 32; ++q) v[q] = 0u;
         }
+        if (c == kChunks - 1) {
+          // accumulator fully read: hand TMEM back to the MMA warp early
+          tc_fence_before();
+          mbar_arrive(&tempty_bar[acc]);
+        }
         float f[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-        uint4* dst = reinterpret_cast<uint4*>(cbase + c * 32);
-        if (p.epilogue == LZ_EPI_GELU) {
-          uint4* adst = reinterpret_cast<uint4*>(abase + c * 32);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) st_v4(adst + q, f32_to_bf16x8(f + 8 * q));
-#pragma unroll
-          for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
-        } else if (p.epilogue == LZ_EPI_DGELU) {
-          const uint4* hsrc = reinterpret_cast<const uint4*>(abase + c * 32);
+        if (dgelu) {
+          mbar_wait(&my_aux_bar[b], aux_phase[b]);
+          aux_phase[b] ^= 1;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             float h[8];
-            bf16x8_to_f32(ld_nc_v4(hsrc + q), h);
+            bf16x8_to_f32(ld_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q)), h);
 #pragma unroll
             for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
           }
         }
+        // the store that used buffer b (chunk c-2) must have finished reading smem
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if (dgelu && c + 2 < kChunks && lane == 0) {
+          fence_async_smem();
+          mbar_expect_tx(&my_aux_bar[b], kEpiBuf);
+          tma_load_2d(wbuf + (2 + b) * kEpiBuf, &map_x, &my_aux_bar[b],
+                      col0 + (c + 2) * kEpiCols, row0);
+        }
+        if (gelu) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) st_v4(dst + q, f32_to_bf16x8(f + 8 * q));
+          for (int q = 0; q < 4; ++q)
+            st_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
+#pragma unroll
+          for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          st_shared_v4(out_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, wbuf + b * kEpiBuf, col0 + c * kEpiCols, row0);
+          if (gelu) tma_store_2d(&map_x, wbuf + (2 + b) * kEpiBuf, col0 + c * kEpiCols, row0);
+          bulk_commit();
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty_bar[acc]);
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
   }
   tc_fence_before();
   __syncthreads();
@@ -418,7 +498,8 @@ static EncodeTiledFn get_encoder() {
 
 // 2D bf16 tensor map over a row-major [outer, inner] matrix, 128B swizzle.
 static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
-                     uint32_t box_inner, uint32_t box_outer) {
+                     uint32_t box_inner, uint32_t box_outer,
+                     CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   EncodeTiledFn enc = get_encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -426,14 +507,14 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int A_MN, int B_MN>
-static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const Params& p, int grid,
-                        cudaStream_t s) {
+static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                        const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -442,7 +523,7 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const Para
       return lzh::check_launch();
     attr_set = true;
   }
-  kern<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, p);
+  kern<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, mx, p);
   return lzh::check_launch();
 }
 
@@ -450,11 +531,12 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
                                      int G, const int32_t* off, int rows_total, int M, int N,
                                      int K, int b_major, int epilogue, int num_sms,
                                      void* stream) {
-  if (G < 1 || G > kMaxGroups || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
+  if (G < 1 || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
+  if (G > kMaxGroups) return LZ_ERR_UNSUPPORTED;
   if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DGELU) return LZ_ERR_ARG;
   if ((epilogue != LZ_EPI_STORE) && (mode != 0 || !aux)) return LZ_ERR_ARG;
   if (N <= 0 || N % BN) return LZ_ERR_UNSUPPORTED;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mc, mx;
   Params p{};
   p.mode = mode;
   p.G = G;
@@ -462,12 +544,11 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.N = N;
   p.K = K;
   p.off = off;
-  p.C = (__nv_bfloat16*)C;
-  p.aux = (__nv_bfloat16*)aux;
   p.epilogue = epilogue;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (rows_total == 0 && mode == 0) return LZ_OK;
+  const CUtensorMapSwizzle sw64 = CU_TENSOR_MAP_SWIZZLE_64B;
   if (mode == 0) {
     if (K <= 0 || K % BK) return LZ_ERR_UNSUPPORTED;
     if (!make_map(&ma, A, K, rows_total, BK, BM)) return LZ_ERR_CUDA;
@@ -476,19 +557,22 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
     } else {
       if (!make_map(&mb, B, N, (uint64_t)G * K, 64, BK)) return LZ_ERR_CUDA;
     }
+    if (!make_map(&mc, C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
+    if (!make_map(&mx, aux ? aux : C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     // upper bound of tiles = rows_total/BM * N/BN; the kernel reads the exact count
     long tiles = (long)(rows_total / BM) * (N / BN);
     int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    return b_major == LZ_K_MAJOR ? launch<0, 0>(ma, mb, p, grid, s)
-                                 : launch<0, 1>(ma, mb, p, grid, s);
+    return b_major == LZ_K_MAJOR ? launch<0, 0>(ma, mb, mc, mx, p, grid, s)
+                                 : launch<0, 1>(ma, mb, mc, mx, p, grid, s);
   } else if (mode == 1) {
     if (M <= 0 || M % BM) return LZ_ERR_UNSUPPORTED;
     const uint64_t rows = rows_total > 0 ? rows_total : 1;
     if (!make_map(&ma, A, M, rows, 64, BK)) return LZ_ERR_CUDA;
     if (!make_map(&mb, B, N, rows, 64, BK)) return LZ_ERR_CUDA;
+    if (!make_map(&mc, C, N, (uint64_t)G * M, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     long tiles = (long)G * (M / BM) * (N / BN);
     int grid = (int)(tiles < sms ? tiles : sms);
-    return launch<1, 1>(ma, mb, p, grid, s);
+    return launch<1, 1>(ma, mb, mc, mc, p, grid, s);
   }
   return LZ_ERR_ARG;
 }
