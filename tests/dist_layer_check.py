@@ -1,0 +1,120 @@
+"""Multi-rank MoE layer check (run under torchrun, one rank per GPU, NCCL):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_layer_check.py [--elastic]
+
+Every rank routes its own tokens through the flexible all-to-all; outputs, input
+grads and the replica-group-summed expert grads are compared with the torch-CPU
+fp32 oracle evaluated on the gathered global batch (tolerances as in
+tests/test_layer_gpu.py).  With --elastic, ranks are then removed (8 -> 6 -> 4 style:
+the highest ranks leave), the host re-plans over the survivors with the reference
+recipe, and the same kernels run the new plan.  Prints "DIST OK" on success.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from oracle import moe_ref  # noqa: E402
+from paper_2407_04656_b200 import ops  # noqa: E402
+from paper_2407_04656_b200.layer import MoELayer, zipf_router_bias  # noqa: E402
+from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix  # noqa: E402
+
+
+def rel(got, ref):
+    got, ref = got.detach().float().cpu(), ref.detach().float().cpu()
+    return float((got - ref).norm() / ref.norm().clamp_min(1e-12))
+
+
+def check(layer, group, Tn, seed, tag):
+    rank, n = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + rank)
+    x = torch.randn(Tn, layer.d, generator=g, device=dev).bfloat16().requires_grad_(True)
+    dout = torch.randn(Tn, layer.d, generator=g, device=dev).bfloat16()
+    layer.zero_grad(set_to_none=True)
+    out = layer(x)
+    out.backward(dout)
+    torch.cuda.synchronize()
+    layer.check()
+    k, E = layer.k, layer.E
+    gidx = ops.router_gate(x.detach(), layer.wg.detach(), layer.bg.detach(), k)[0]
+    # gather the global batch on every rank
+    xs = [torch.empty_like(x.detach()) for _ in range(n)]
+    ds = [torch.empty_like(dout) for _ in range(n)]
+    ids = [torch.empty_like(gidx) for _ in range(n)]
+    dist.all_gather(xs, x.detach().contiguous(), group=group)
+    dist.all_gather(ds, dout, group=group)
+    dist.all_gather(ids, gidx, group=group)
+    # full weights: every owner holds the deterministic per-expert init (no optimizer step)
+    from paper_2407_04656_b200.layer import _expert_weights
+    w1 = torch.stack([_expert_weights(layer.seed, 2 * e, (layer.d_ff, layer.d), layer.init_std, dev)
+                      for e in range(E)]).float().cpu().requires_grad_(True)
+    w2 = torch.stack([_expert_weights(layer.seed, 2 * e + 1, (layer.d, layer.d_ff), layer.init_std,
+                                      dev) for e in range(E)]).float().cpu().requires_grad_(True)
+    for p, e in enumerate(layer.local_ids):
+        assert torch.equal(layer.w1.detach()[p].float().cpu(), w1.detach()[e]), f"expert {e} copy"
+    X = torch.cat([t.float().cpu() for t in xs]).requires_grad_(True)
+    wg = layer.wg.detach().float().cpu().requires_grad_(True)
+    bg = layer.bg.detach().float().cpu().requires_grad_(True)
+    ref, _, _, _ = moe_ref.moe_forward_ref(X, wg, bg, w1, w2, k, layer.renorm,
+                                           idx=torch.cat([t.cpu() for t in ids]))
+    ref.backward(torch.cat([t.float().cpu() for t in ds]))
+    sl = slice(rank * Tn, (rank + 1) * Tn)
+    errs = {"out": rel(out, ref[sl]), "dx": rel(x.grad, X.grad[sl]), "dwg": rel(layer.wg.grad, wg.grad),
+            "dbg": rel(layer.bg.grad, bg.grad)}
+    for p, e in enumerate(layer.local_ids):
+        errs[f"dW1[{e}]"] = rel(layer.w1.grad[p], w1.grad[e])
+        errs[f"dW2[{e}]"] = rel(layer.w2.grad[p], w2.grad[e])
+    bad = {kk: v for kk, v in errs.items() if v > (5e-2 if kk in ("dwg", "dbg") else 3e-2)}
+    print(f"[{tag}] rank {rank}/{n} local experts {layer.local_ids} imbalance "
+          f"{layer.imbalance():.3f} max rel err {max(errs.values()):.3e}", flush=True)
+    assert not bad, f"rank {rank}: {bad}"
+
+
+def main():
+    elastic = "--elastic" in sys.argv
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, n = dist.get_rank(), dist.get_world_size()
+    E, k, d, dff, Tn = 8, 2, 512, 1024, 2048
+    bias = zipf_router_bias(E, 1.2, seed=2)
+    loads = (torch.softmax(bias, 0) * Tn * n * k).round().long().clamp_min(1).tolist()
+    c = math.ceil(3 * E / n)
+    R = replica_matrix(plan_for_loads(loads, n, c, 2))
+    layer = MoELayer(d, dff, E, k, replicas=R, group=dist.group.WORLD, seed=7, init_std=0.05,
+                     router_bias=bias)
+    check(layer, dist.group.WORLD, Tn, 100, f"N={n}")
+    group = dist.group.WORLD
+    if elastic and n > 2:
+        from paper_2407_04656_b200.elastic import shrink_and_replan
+        # 8 -> 6 -> 4 when launched on 8 GPUs (4 -> 3 -> 2 on 4): drop two ranks, twice
+        step = max(1, n // 4)
+        for _ in range(2):
+            cur = dist.get_world_size(group)
+            if cur - step < 2:
+                break
+            exclude = list(range(cur - step, cur))
+            if dist.get_rank(group) in exclude:
+                print(f"rank {rank} leaves (simulated failure)", flush=True)
+                os._exit(0)
+            layer, group, rep = shrink_and_replan(layer, group, exclude, loads, c)
+            if dist.get_rank(group) == 0:
+                print(f"re-plan: {rep}", flush=True)
+            check(layer, group, Tn, 200 + cur, f"N={dist.get_world_size(group)} after failure")
+    dist.barrier(group=group)
+    if dist.get_rank(group) == 0:
+        print("DIST OK", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
