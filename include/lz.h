@@ -76,6 +76,7 @@ lz_status lz_plan_workspace_bytes(int E, int N, int P, size_t* bytes);
  *   gather[P] local assignment at send slot s            (= build_shuffle_index result)
  *   dest_row[P] row of assignment p in its destination rank's expert-major receive
  *             buffer (segments padded to `align` rows, source-major inside an expert)
+ *   dest_rank[P] (optional) the destination rank j of assignment p
  *   recv_m[E]        tokens of expert e this rank receives (incl. self)   (received[j][e][:] sum, :276-282)
  *   recv_off[E+1]    padded expert-major offsets of this rank's receive buffer
  *   recv_src_off[E*N] row where source i's tokens of expert e start on this rank
@@ -86,10 +87,10 @@ lz_status lz_plan_workspace_bytes(int E, int N, int P, size_t* bytes);
 lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E, int N, int rank,
                            const int32_t* routed, int P, int align, int64_t* quota, int32_t* D,
                            int32_t* send_sizes, int32_t* recv_sizes, int32_t* recv_counts,
-                           int32_t* slot, int32_t* gather, int32_t* dest_row, int32_t* recv_m,
-                           int32_t* recv_off, int32_t* recv_src_off, int32_t* recv_stage_off,
-                           int32_t* recv_cnt, int32_t* err, void* ws, size_t ws_bytes,
-                           void* stream);
+                           int32_t* slot, int32_t* gather, int32_t* dest_row, int32_t* dest_rank,
+                           int32_t* recv_m, int32_t* recv_off, int32_t* recv_src_off,
+                           int32_t* recv_stage_off, int32_t* recv_cnt, int32_t* err, void* ws,
+                           size_t ws_bytes, void* stream);
 
 /* Replaces build_shuffle_index (dispatch.py:199-237) given only a schedule's
  * send_counts (E x N, = DispatchSchedule.send_counts): slot[P] and gather[P] as above;
@@ -134,6 +135,28 @@ lz_status lz_copy_segments(const void* in, void* out, int d, int nseg, const int
 /* out[t] = sum_s w[t,s] * y[row[t*k+s]]  (fixed s order, fp32 accumulate, bf16 out). */
 lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, int d, int k,
                      void* out, void* stream);
+
+/* ------------------------------------- fused dispatch/combine over NVLink peers */
+/* Variants of pack / combine / combine_bwd / dispatch_bwd that move rows straight to
+ * or from the destination rank's symmetric receive buffer through NVLink P2P
+ * (`peers*[N]`: device array of each rank's buffer base address, e.g. from torch
+ * symmetric memory), replacing send-buffer + NCCL all-to-all-v + regroup.  The caller
+ * orders them with a cross-rank barrier (writes complete before the peer reads). */
+lz_status lz_pack_p2p(const void* x, int Tn, int d, int k, const int32_t* dest_rank,
+                      const int32_t* dest_row, const unsigned long long* peers, void* own, int E,
+                      const int32_t* recv_m, const int32_t* recv_off, void* stream);
+lz_status lz_combine_p2p(const unsigned long long* peers_y, const int32_t* dest_rank,
+                         const int32_t* dest_row, const float* w, int Tn, int d, int k, void* out,
+                         void* stream);
+lz_status lz_combine_bwd_p2p(const void* dout, const unsigned long long* peers_y,
+                             const unsigned long long* peers_dy, const int32_t* dest_rank,
+                             const int32_t* dest_row, const float* w, int Tn, int d, int k,
+                             float* dw, void* own_dy, int E, const int32_t* recv_m,
+                             const int32_t* recv_off, void* stream);
+lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe, const int32_t* dest_rank,
+                              const int32_t* dest_row, int Tn, int d, int k, const float* probs,
+                              const int32_t* idx, const float* dw, const void* wg, int E,
+                              int renorm, void* dx, float* dlogits, void* stream);
 
 /* -------------------------------------------------------------- K8 backward */
 

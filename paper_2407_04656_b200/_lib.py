@@ -20,8 +20,13 @@ _SIGS = {
     "lz_plan_matrices": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp],
     "lz_plan_workspace_bytes": [_i, _i, _i, ctypes.POINTER(ctypes.c_size_t)],
     # T R E N rank routed P align | quota D send recv recv_counts slot gather dest_row
-    # recv_m recv_off recv_src_off recv_stage_off recv_cnt err ws | ws_bytes stream
-    "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i] + [_vp] * 15 + [_sz, _vp],
+    # dest_rank recv_m recv_off recv_src_off recv_stage_off recv_cnt err ws | ws_bytes stream
+    "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i] + [_vp] * 16 + [_sz, _vp],
+    "lz_pack_p2p": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp],
+    "lz_combine_p2p": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp],
+    "lz_combine_bwd_p2p": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
+    "lz_dispatch_bwd_p2p": [_vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _i, _vp, _vp,
+                            _vp],
     "lz_shuffle_index": [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp],
     "lz_gate_topk": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "lz_router_gate": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
@@ -83,7 +88,8 @@ def exported_symbols() -> list[str]:
 _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
             "lz_gate_topk": 1, "lz_router_gate": 1, "lz_invert_permutation": 1, "lz_pack": 1,
             "lz_copy_segments": 1, "lz_combine": 1, "lz_combine_bwd": 1, "lz_dispatch_bwd": 1,
-            "lz_router_wgrad": 2, "lz_grouped_gemm": 1}
+            "lz_router_wgrad": 2, "lz_grouped_gemm": 1, "lz_pack_p2p": 1, "lz_combine_p2p": 1,
+            "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1}
 launch_count = 0
 
 

@@ -45,6 +45,39 @@ def all_to_all_rows(out: torch.Tensor, inp: torch.Tensor, out_splits: Sequence[i
     return out
 
 
+class SymmetricRows:
+    """``nbuf`` row buffers [rows, d] (bf16) allocated in NVLink-mapped symmetric memory
+    (torch symmetric memory: cuMem + IPC handles, one mapping per peer).  ``peers(b)``
+    is a device int64 [N] array of every rank's address of buffer b, consumed by the
+    fused P2P dispatch/combine kernels; ``barrier()`` is a device-side cross-rank
+    barrier on the current stream (orders P2P writes before the peers read)."""
+
+    def __init__(self, group, nbuf: int, rows: int, d: int, device):
+        import torch.distributed._symmetric_memory as symm
+        try:
+            symm.enable_symm_mem_for_group(group.group_name)
+        except Exception:
+            pass
+        self.rows, self.d, self.nbuf = rows, d, nbuf
+        self.t = symm.empty((nbuf, rows, d), dtype=torch.bfloat16, device=device)
+        self.h = symm.rendezvous(self.t, group)
+        n = self.h.world_size
+        base = [self.h.get_remote_tensor(r, (nbuf, rows, d), torch.bfloat16).data_ptr()
+                for r in range(n)]
+        stride = rows * d * 2
+        self.ptrs = torch.tensor([[b + i * stride for b in base] for i in range(nbuf)],
+                                 dtype=torch.int64, device=device)
+
+    def buf(self, i: int) -> torch.Tensor:
+        return self.t[i]
+
+    def peers(self, i: int) -> torch.Tensor:
+        return self.ptrs[i]
+
+    def barrier(self) -> None:
+        self.h.barrier(channel=0)
+
+
 def owner_sets(R: Sequence[Sequence[int]]) -> list[tuple[int, ...]]:
     """owners[e] = ranks hosting at least one replica of expert e."""
     return [tuple(j for j, v in enumerate(row) if v > 0) for row in R]

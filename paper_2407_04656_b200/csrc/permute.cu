@@ -32,8 +32,18 @@ __device__ __forceinline__ void zero_pad_rows(void* out, int d, int E, const int
   }
 }
 
+// Row base for assignment slot s of the current token: a peer's symmetric buffer
+// (NVLink P2P, `peers[rank]`) when `peers` is given, else the local buffer.
+__device__ __forceinline__ uint4* row_base(uint4* local, const unsigned long long* peers,
+                                           int my_rk, int s) {
+  if (!peers) return local;
+  const int r = __shfl_sync(0xffffffffu, my_rk, s);
+  return reinterpret_cast<uint4*>(peers[r]);
+}
+
 __global__ void __launch_bounds__(kRowThreads) pack_kernel(
     const uint4* __restrict__ x, int Tn, int d, int k, const int32_t* __restrict__ row,
+    const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers,
     uint4* __restrict__ out, int E, const int32_t* __restrict__ recv_m,
     const int32_t* __restrict__ recv_off, long n_pad_items) {
   const int lane = threadIdx.x % 32;
@@ -46,6 +56,7 @@ __global__ void __launch_bounds__(kRowThreads) pack_kernel(
       continue;
     }
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
     const uint4* src = x + t * nch;
     for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
       uint4 v[kVec];
@@ -54,7 +65,7 @@ __global__ void __launch_bounds__(kRowThreads) pack_kernel(
         if (c0 + 32 * u < nch) v[u] = ld_nc_v4(src + c0 + 32 * u);
       for (int s = 0; s < k; ++s) {
         const long r = __shfl_sync(0xffffffffu, my_row, s);
-        uint4* dst = out + r * nch;
+        uint4* dst = row_base(out, peers, my_rk, s) + r * nch;
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
           if (c0 + 32 * u < nch) st_v4(dst + c0 + 32 * u, v[u]);
@@ -63,11 +74,10 @@ __global__ void __launch_bounds__(kRowThreads) pack_kernel(
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads) combine_kernel(const uint4* __restrict__ y,
-                                                              const int32_t* __restrict__ row,
-                                                              const float* __restrict__ w,
-                                                              int Tn, int d, int k,
-                                                              uint4* __restrict__ out) {
+__global__ void __launch_bounds__(kRowThreads) combine_kernel(
+    const uint4* __restrict__ y, const int32_t* __restrict__ row, const int32_t* __restrict__ prank,
+    const unsigned long long* __restrict__ peers, const float* __restrict__ w, int Tn, int d, int k,
+    uint4* __restrict__ out) {
   const int lane = threadIdx.x % 32;
   const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
   const long nw = (long)gridDim.x * kRowWarps;
@@ -75,6 +85,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const uint4* __res
   for (long t = gw; t < Tn; t += nw) {
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
     const float my_w = lane < k ? __ldg(w + t * k + lane) : 0.f;
+    const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
     for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
       float acc[kVec][8];
 #pragma unroll
@@ -84,7 +95,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const uint4* __res
       for (int s = 0; s < k; ++s) {
         const long r = __shfl_sync(0xffffffffu, my_row, s);
         const float ws = __shfl_sync(0xffffffffu, my_w, s);
-        const uint4* src = y + r * nch;
+        const uint4* src = row_base(const_cast<uint4*>(y), peers, my_rk, s) + r * nch;
         uint4 v[kVec];
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
@@ -108,6 +119,8 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(const uint4* __res
 
 __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
     const uint4* __restrict__ dout, const uint4* __restrict__ y, const int32_t* __restrict__ row,
+    const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers_y,
+    const unsigned long long* __restrict__ peers_dy,
     const float* __restrict__ w, int Tn, int d, int k, uint4* __restrict__ dy,
     float* __restrict__ dw, int E, const int32_t* __restrict__ recv_m,
     const int32_t* __restrict__ recv_off, long n_pad_items) {
@@ -122,6 +135,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
     }
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
     const float my_w = lane < k ? __ldg(w + t * k + lane) : 0.f;
+    const int my_rk = (peers_y && lane < k) ? __ldg(prank + t * k + lane) : 0;
     float dot[LZ_MAX_TOPK];
 #pragma unroll
     for (int s = 0; s < LZ_MAX_TOPK; ++s) dot[s] = 0.f;
@@ -135,10 +149,12 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
         if (s >= k) break;
         const long r = __shfl_sync(0xffffffffu, my_row, s);
         const float ws = __shfl_sync(0xffffffffu, my_w, s);
+        const uint4* ys = row_base(const_cast<uint4*>(y), peers_y, my_rk, s) + r * nch;
+        uint4* dys = row_base(dy, peers_dy, my_rk, s) + r * nch;
         uint4 v[kVec];
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
-          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(y + r * nch + c0 + 32 * u);
+          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(ys + c0 + 32 * u);
 #pragma unroll
         for (int u = 0; u < kVec; ++u) {
           if (c0 + 32 * u < nch) {
@@ -149,7 +165,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
               dot[s] = fmaf(g[u][q], f[q], dot[s]);
               o[q] = ws * g[u][q];
             }
-            st_v4(dy + r * nch + c0 + 32 * u, f32_to_bf16x8(o));
+            st_v4(dys + c0 + 32 * u, f32_to_bf16x8(o));
           }
         }
       }
@@ -165,8 +181,9 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
 
 // Gate backward (softmax + top-k (+renorm)) and dispatch backward, one warp per token.
 __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
-    const uint4* __restrict__ dxe, const int32_t* __restrict__ row, int Tn, int d, int k,
-    const float* __restrict__ probs, const int32_t* __restrict__ idx,
+    const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
+    const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
+    int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
     const float* __restrict__ dwv, const uint4* __restrict__ wg, int E, int renorm,
     uint4* __restrict__ dx, float* __restrict__ dlogits) {
   const int lane = threadIdx.x % 32;
@@ -177,6 +194,7 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
     const int my_idx = lane < k ? __ldg(idx + t * k + lane) : -1;
     const float my_dw = lane < k ? __ldg(dwv + t * k + lane) : 0.f;
+    const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
     // lane owns experts e = lane and e = lane + 32 (E <= 64)
     float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
 #pragma unroll
@@ -222,10 +240,11 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
         for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
       for (int s = 0; s < k; ++s) {
         const long r = __shfl_sync(0xffffffffu, my_row, s);
+        const uint4* src = row_base(const_cast<uint4*>(dxe), peers, my_rk, s) + r * nch;
         uint4 v[kVec];
 #pragma unroll
         for (int u = 0; u < kVec; ++u)
-          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(dxe + r * nch + c0 + 32 * u);
+          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(src + c0 + 32 * u);
 #pragma unroll
         for (int u = 0; u < kVec; ++u) {
           if (c0 + 32 * u < nch) {
@@ -372,26 +391,70 @@ static long pad_items(int E, const int32_t* recv_m, const int32_t* recv_off, int
 // items to cover the worst case of (align-1) pad rows per expert, align = 128.
 static constexpr int kPadAlign = 128;
 
-extern "C" lz_status lz_pack(const void* x, int Tn, int d, int k, const int32_t* row, void* out,
-                             int E, const int32_t* recv_m, const int32_t* recv_off,
-                             void* stream) {
+static lz_status pack_impl(const void* x, int Tn, int d, int k, const int32_t* row,
+                           const int32_t* prank, const unsigned long long* peers, void* out, int E,
+                           const int32_t* recv_m, const int32_t* recv_off, void* stream) {
   if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
   if (Tn > 0 && (!x || !row || !out)) return LZ_ERR_ARG;
   if (E > 0 && (!recv_m || !recv_off || !out)) return LZ_ERR_ARG;
   const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
   if (Tn + npad == 0) return LZ_OK;
   pack_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, Tn, d, k, row, (uint4*)out, E, recv_m, recv_off, npad);
+      (const uint4*)x, Tn, d, k, row, prank, peers, (uint4*)out, E, recv_m, recv_off, npad);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_pack(const void* x, int Tn, int d, int k, const int32_t* row, void* out,
+                             int E, const int32_t* recv_m, const int32_t* recv_off,
+                             void* stream) {
+  return pack_impl(x, Tn, d, k, row, nullptr, nullptr, out, E, recv_m, recv_off, stream);
+}
+
+extern "C" lz_status lz_pack_p2p(const void* x, int Tn, int d, int k, const int32_t* dest_rank,
+                                 const int32_t* dest_row, const unsigned long long* peers,
+                                 void* own, int E, const int32_t* recv_m,
+                                 const int32_t* recv_off, void* stream) {
+  if (!peers || !dest_rank) return LZ_ERR_ARG;
+  return pack_impl(x, Tn, d, k, dest_row, dest_rank, peers, own, E, recv_m, recv_off, stream);
+}
+
+static lz_status combine_impl(const void* y, const int32_t* row, const int32_t* prank,
+                              const unsigned long long* peers, const float* w, int Tn, int d,
+                              int k, void* out, void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK) return LZ_ERR_ARG;
+  if (Tn == 0) return LZ_OK;
+  if ((!y && !peers) || !row || !w || !out) return LZ_ERR_ARG;
+  combine_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)y, row, prank, peers, w, Tn, d, k, (uint4*)out);
   return lzh::check_launch();
 }
 
 extern "C" lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, int d,
                                 int k, void* out, void* stream) {
-  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK) return LZ_ERR_ARG;
-  if (Tn == 0) return LZ_OK;
-  if (!y || !row || !w || !out) return LZ_ERR_ARG;
-  combine_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)y, row, w, Tn, d, k, (uint4*)out);
+  return combine_impl(y, row, nullptr, nullptr, w, Tn, d, k, out, stream);
+}
+
+extern "C" lz_status lz_combine_p2p(const unsigned long long* peers_y, const int32_t* dest_rank,
+                                    const int32_t* dest_row, const float* w, int Tn, int d,
+                                    int k, void* out, void* stream) {
+  if (!peers_y || !dest_rank) return LZ_ERR_ARG;
+  return combine_impl(nullptr, dest_row, dest_rank, peers_y, w, Tn, d, k, out, stream);
+}
+
+static lz_status combine_bwd_impl(const void* dout, const void* y, const int32_t* row,
+                                  const int32_t* prank, const unsigned long long* peers_y,
+                                  const unsigned long long* peers_dy, const float* w, int Tn,
+                                  int d, int k, void* dy, float* dw, int E,
+                                  const int32_t* recv_m, const int32_t* recv_off, void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
+  if (Tn > 0 && (!dout || (!y && !peers_y) || !row || !w || (!dy && !peers_dy) || !dw))
+    return LZ_ERR_ARG;
+  if (E > 0 && (!recv_m || !recv_off || !dy)) return LZ_ERR_ARG;
+  const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
+  if (Tn + npad == 0) return LZ_OK;
+  combine_bwd_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dout, (const uint4*)y, row, prank, peers_y, peers_dy, w, Tn, d, k, (uint4*)dy,
+      dw, E, recv_m, recv_off, npad);
   return lzh::check_launch();
 }
 
@@ -399,14 +462,33 @@ extern "C" lz_status lz_combine_bwd(const void* dout, const void* y, const int32
                                     const float* w, int Tn, int d, int k, void* dy, float* dw,
                                     int E, const int32_t* recv_m, const int32_t* recv_off,
                                     void* stream) {
-  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
-  if (Tn > 0 && (!dout || !y || !row || !w || !dy || !dw)) return LZ_ERR_ARG;
-  if (E > 0 && (!recv_m || !recv_off || !dy)) return LZ_ERR_ARG;
-  const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
-  if (Tn + npad == 0) return LZ_OK;
-  combine_bwd_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dout, (const uint4*)y, row, w, Tn, d, k, (uint4*)dy, dw, E, recv_m, recv_off,
-      npad);
+  return combine_bwd_impl(dout, y, row, nullptr, nullptr, nullptr, w, Tn, d, k, dy, dw, E, recv_m,
+                          recv_off, stream);
+}
+
+extern "C" lz_status lz_combine_bwd_p2p(const void* dout, const unsigned long long* peers_y,
+                                        const unsigned long long* peers_dy,
+                                        const int32_t* dest_rank, const int32_t* dest_row,
+                                        const float* w, int Tn, int d, int k, float* dw,
+                                        void* own_dy, int E, const int32_t* recv_m,
+                                        const int32_t* recv_off, void* stream) {
+  if (!peers_y || !peers_dy || !dest_rank) return LZ_ERR_ARG;
+  return combine_bwd_impl(dout, nullptr, dest_row, dest_rank, peers_y, peers_dy, w, Tn, d, k,
+                          own_dy, dw, E, recv_m, recv_off, stream);
+}
+
+static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const int32_t* prank,
+                                   const unsigned long long* peers, int Tn, int d, int k,
+                                   const float* probs, const int32_t* idx, const float* dw,
+                                   const void* wg, int E, int renorm, void* dx, float* dlogits,
+                                   void* stream) {
+  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 1 || E > 64)
+    return LZ_ERR_ARG;
+  if (Tn == 0) return LZ_OK;
+  if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
+  dispatch_bwd_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const uint4*)wg, E, renorm,
+      (uint4*)dx, dlogits);
   return lzh::check_launch();
 }
 
@@ -414,14 +496,19 @@ extern "C" lz_status lz_dispatch_bwd(const void* dxe, const int32_t* row, int Tn
                                      const float* probs, const int32_t* idx, const float* dw,
                                      const void* wg, int E, int renorm, void* dx,
                                      float* dlogits, void* stream) {
-  if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 1 || E > 64)
-    return LZ_ERR_ARG;
-  if (Tn == 0) return LZ_OK;
-  if (!dxe || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
-  dispatch_bwd_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dxe, row, Tn, d, k, probs, idx, dw, (const uint4*)wg, E, renorm, (uint4*)dx,
-      dlogits);
-  return lzh::check_launch();
+  return dispatch_bwd_impl(dxe, row, nullptr, nullptr, Tn, d, k, probs, idx, dw, wg, E, renorm, dx,
+                           dlogits, stream);
+}
+
+extern "C" lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe,
+                                         const int32_t* dest_rank, const int32_t* dest_row,
+                                         int Tn, int d, int k, const float* probs,
+                                         const int32_t* idx, const float* dw, const void* wg,
+                                         int E, int renorm, void* dx, float* dlogits,
+                                         void* stream) {
+  if (!peers_dxe || !dest_rank) return LZ_ERR_ARG;
+  return dispatch_bwd_impl(nullptr, dest_row, dest_rank, peers_dxe, Tn, d, k, probs, idx, dw, wg,
+                           E, renorm, dx, dlogits, stream);
 }
 
 static int wgrad_nblk(int Tn) {

@@ -249,7 +249,8 @@ __global__ void __launch_bounds__(kSlotThreads) slot_kernel(
     const int32_t* __restrict__ routed, int P, int E, int N, int B,
     const int32_t* __restrict__ blk_base, const int32_t* __restrict__ tab_pref,
     const int32_t* __restrict__ tab_sdelta, const int32_t* __restrict__ tab_ddelta,
-    int32_t* __restrict__ slot, int32_t* __restrict__ gather, int32_t* __restrict__ dest_row) {
+    int32_t* __restrict__ slot, int32_t* __restrict__ gather, int32_t* __restrict__ dest_row,
+    int32_t* __restrict__ dest_rank) {
   extern __shared__ int32_t s_cnt[];  // [kSlotWarps][E]
   const int b = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -291,6 +292,7 @@ __global__ void __launch_bounds__(kSlotThreads) slot_kernel(
       slot[p] = s;
       gather[s] = p;
       if (dest_row) dest_row[p] = m + tab_ddelta[e * N + j];
+      if (dest_rank) dest_rank[p] = j;
     }
     __syncwarp();
     if (e >= 0 && (peers & lt) == 0) s_cnt[warp * E + e] += __popc(peers);
@@ -329,7 +331,8 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
                                       const int32_t* routed, int P, int align, int64_t* quota,
                                       int32_t* D, int32_t* send_sizes, int32_t* recv_sizes,
                                       int32_t* recv_counts, int32_t* slot, int32_t* gather,
-                                      int32_t* dest_row, int32_t* recv_m, int32_t* recv_off,
+                                      int32_t* dest_row, int32_t* dest_rank, int32_t* recv_m,
+                                      int32_t* recv_off,
                                       int32_t* recv_src_off, int32_t* recv_stage_off,
                                       int32_t* recv_cnt, int32_t* err, void* ws,
                                       size_t ws_bytes, void* stream) {
@@ -367,7 +370,7 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
   if ((st = lzh::check_launch()) != LZ_OK) return st;
   if (P > 0) {
     slot_kernel<<<B, kSlotThreads, sizeof(int32_t) * kSlotWarps * E, s>>>(
-        routed, P, E, N, B, blk_base, pref, sdelta, ddelta, slot, gather, dest_row);
+        routed, P, E, N, B, blk_base, pref, sdelta, ddelta, slot, gather, dest_row, dest_rank);
     if ((st = lzh::check_launch()) != LZ_OK) return st;
   }
   return LZ_OK;
@@ -464,7 +467,7 @@ extern "C" lz_status lz_shuffle_index(const int32_t* send_counts, int E, int N,
   if ((st = lzh::check_launch()) != LZ_OK) return st;
   if (P > 0) {
     slot_kernel<<<B, kSlotThreads, sizeof(int32_t) * kSlotWarps * E, s>>>(
-        routed, P, E, N, B, blk_base, pref, sdelta, sdelta, slot, gather, nullptr);
+        routed, P, E, N, B, blk_base, pref, sdelta, sdelta, slot, gather, nullptr, nullptr);
     if ((st = lzh::check_launch()) != LZ_OK) return st;
   }
   return LZ_OK;

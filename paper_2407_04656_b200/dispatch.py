@@ -205,6 +205,7 @@ class DevicePlan(NamedTuple):
     slot: torch.Tensor         # int32 [P]  send slot of assignment p
     gather: torch.Tensor       # int32 [P]  assignment at send slot s
     dest_row: torch.Tensor     # int32 [P]  row in the destination's expert-major buffer
+    dest_rank: torch.Tensor    # int32 [P]  destination rank
     recv_m: torch.Tensor       # int32 [E]
     recv_off: torch.Tensor     # int32 [E+1] padded expert-major offsets (this rank)
     recv_src_off: torch.Tensor  # int32 [E, N]
@@ -231,6 +232,7 @@ def plan_device(T: torch.Tensor, R: torch.Tensor, rank: int, routed: torch.Tenso
     slot = torch.empty(P, **i32)
     gather = torch.empty(P, **i32)
     dest_row = torch.empty(P, **i32)
+    dest_rank = torch.empty(P, **i32)
     recv_m = torch.empty(E, **i32)
     recv_off = torch.empty(E + 1, **i32)
     recv_src_off, recv_stage_off, recv_cnt = (torch.empty((E, N), **i32) for _ in range(3))
@@ -240,11 +242,12 @@ def plan_device(T: torch.Tensor, R: torch.Tensor, rank: int, routed: torch.Tenso
               _lib.ptr(routed) if P else None, P, align, _lib.ptr(quota), _lib.ptr(D),
               _lib.ptr(send_sizes), _lib.ptr(recv_sizes), _lib.ptr(recv_counts),
               _lib.ptr(slot) if P else None, _lib.ptr(gather) if P else None,
-              _lib.ptr(dest_row) if P else None, _lib.ptr(recv_m), _lib.ptr(recv_off),
+              _lib.ptr(dest_row) if P else None, _lib.ptr(dest_rank) if P else None,
+              _lib.ptr(recv_m), _lib.ptr(recv_off),
               _lib.ptr(recv_src_off), _lib.ptr(recv_stage_off), _lib.ptr(recv_cnt),
               _lib.ptr(err), _lib.ptr(ws), ws.numel(), _lib.stream_ptr(stream))
     return DevicePlan(quota, D, send_sizes, recv_sizes, recv_counts, slot, gather, dest_row,
-                      recv_m, recv_off, recv_src_off, recv_stage_off, recv_cnt, err)
+                      dest_rank, recv_m, recv_off, recv_src_off, recv_stage_off, recv_cnt, err)
 
 
 # ------------------------------------------------------- reference API

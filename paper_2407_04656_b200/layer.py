@@ -22,6 +22,7 @@ surfaced by :meth:`MoELayer.check`.
 from __future__ import annotations
 
 import math
+import os
 from typing import Sequence
 
 import torch
@@ -43,7 +44,7 @@ def _expert_weights(seed: int, e: int, shape, std: float, device) -> torch.Tenso
 class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int = 2, *,
                  replicas=None, group=None, renorm: bool = False, seed: int = 0,
-                 init_std: float = 0.02, router_bias=None, device=None):
+                 init_std: float = 0.02, router_bias=None, device=None, exchange: str | None = None):
         super().__init__()
         if d_model % 256 or d_ff % 256:
             raise ValueError("d_model and d_ff must be multiples of 256 (GEMM tile)")
@@ -67,6 +68,10 @@ class MoELayer(torch.nn.Module):
         self.w1 = None
         self.w2 = None
         self.last_plan: DevicePlan | None = None
+        self.exchange = exchange or os.environ.get("LZ_EXCHANGE", "p2p")
+        self._symm = None
+        self._symm_group = None
+        self._fwd_version = 0
         self.set_plan(replicas)
 
     # ------------------------------------------------------------- plan
@@ -112,6 +117,23 @@ class MoELayer(torch.nn.Module):
         self.w2 = torch.nn.Parameter(torch.stack(w2s).contiguous())
         self.replica_groups = comm.ReplicaGroups(R, self.group) if self.world > 1 else None
 
+    def exchange_mode(self) -> str:
+        """'local' (N = 1), 'p2p' (fused NVLink dispatch/combine through symmetric memory,
+        the default for N > 1) or 'nccl' (send buffer + NCCL all-to-all-v + regroup)."""
+        if self.world == 1:
+            return "local"
+        return self.exchange
+
+    def symmetric(self, Tn: int):
+        """Symmetric X / Y / dY / dX receive buffers sized for the worst case (every
+        rank's P assignments landing on one rank) -- no host round trip is ever needed
+        to size them; 180 GB of HBM makes the bound affordable."""
+        rows = _capacity(self.world * Tn * self.k + self.E * (ALIGN - 1))
+        if self._symm is None or self._symm.rows < rows or self._symm_group is not self.group:
+            self._symm = comm.SymmetricRows(self.group, 4, rows, self.d, self.device)
+            self._symm_group = self.group
+        return self._symm
+
     def expert_state(self) -> dict:
         return {e: (self.w1.data[p], self.w2.data[p]) for p, e in enumerate(self.local_ids)}
 
@@ -146,23 +168,33 @@ class _MoEFunction(torch.autograd.Function):
         Tn, d = x.shape
         k, E, G = layer.k, layer.E, len(layer.local_ids)
         N, rank, group = layer.world, layer.rank, layer.group
+        mode = layer.exchange_mode()
         idx, w, probs, hist = ops.router_gate(x, wg, bg, k, layer.renorm)
         T = comm.allgather_hist(hist, group)
         plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ALIGN)
         layer.last_plan = plan
         off = plan.recv_off.index_select(0, layer._off_index).contiguous()
         P = Tn * k
-        if N == 1:
+        sizes = None
+        if mode == "local":
             cap = _capacity(P + E * (ALIGN - 1))
             X = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
+            Y = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
             ops.pack(x, plan.dest_row, k, X, plan.recv_m, plan.recv_off)
-            sizes = None
+        elif mode == "p2p":
+            # fused dispatch: rows go straight into the destination's symmetric buffer
+            sym = layer.symmetric(Tn)
+            layer._fwd_version += 1
+            cap = sym.rows
+            X, Y = sym.buf(0), sym.buf(1)
+            ops.pack_p2p(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X, plan.recv_m,
+                         plan.recv_off)
+            sym.barrier()
         else:
-            # v1 exchange: one D2H of the counts (+ error flag) per layer forward
+            # NCCL exchange: one D2H of the counts (+ error flag) per layer forward
             host = torch.cat([plan.send_sizes, plan.recv_counts, plan.err,
                               plan.recv_cnt.max().view(1)]).cpu()
-            err = int(host[2 * N])
-            if err:
+            if int(host[2 * N]):
                 plan.check()
             send_sizes = host[:N].tolist()
             recv_counts = host[N:2 * N].tolist()
@@ -175,6 +207,7 @@ class _MoEFunction(torch.autograd.Function):
             stage = torch.empty((n_recv, d), dtype=torch.bfloat16, device=x.device)
             comm.all_to_all_rows(stage, send, recv_counts, send_sizes, group)
             X = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
+            Y = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
             ops.zero_pad_rows(X, plan.recv_m, plan.recv_off)
             ops.copy_segments(stage, X, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
                               max_seg)
@@ -182,12 +215,15 @@ class _MoEFunction(torch.autograd.Function):
         d_ff = layer.d_ff
         H = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
         A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
-        Y = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
         if G > 0:
             ops.grouped_gemm_rows(X, w1, off, A, epilogue=_lib.LZ_EPI_GELU, aux=H)
             ops.grouped_gemm_rows(A, w2, off, Y)
-        if N == 1:
+        if mode == "local":
             out = ops.combine(Y, plan.dest_row, w, k)
+            ret, row = Y, plan.dest_row
+        elif mode == "p2p":
+            sym.barrier()
+            out = ops.combine_p2p(sym.peers(1), plan.dest_rank, plan.dest_row, w, k, d)
             ret, row = Y, plan.dest_row
         else:
             send_sizes, recv_counts, max_seg = sizes
@@ -199,7 +235,7 @@ class _MoEFunction(torch.autograd.Function):
             out = ops.combine(ret, plan.slot, w, k)
             row = plan.slot
         ctx.layer = layer
-        ctx.meta = (Tn, cap, sizes)
+        ctx.meta = (Tn, cap, sizes, mode, layer._fwd_version)
         ctx.plan = plan
         ctx.save_for_backward(x, wg, w1, w2, idx, w, probs, off, X, H, A, ret, row)
         return out
@@ -209,15 +245,25 @@ class _MoEFunction(torch.autograd.Function):
         layer: MoELayer = ctx.layer
         x, wg, w1, w2, idx, w, probs, off, X, H, A, ret, row = ctx.saved_tensors
         plan: DevicePlan = ctx.plan
-        Tn, cap, sizes = ctx.meta
+        Tn, cap, sizes, mode, version = ctx.meta
         k, N, group = layer.k, layer.world, layer.group
         d, d_ff = layer.d, layer.d_ff
         G = len(layer.local_ids)
         dout = dout.contiguous().to(torch.bfloat16)
         dev = x.device
-        if N == 1:
+        if mode == "local":
             dY = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
+            dX = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
             dw = ops.combine_bwd(dout, ret, row, w, k, dY, plan.recv_m, plan.recv_off)
+        elif mode == "p2p":
+            if version != layer._fwd_version:
+                raise RuntimeError("P2P exchange keeps one forward in flight per layer: "
+                                   "run backward before the next forward")
+            sym = layer.symmetric(Tn)
+            dY, dX = sym.buf(2), sym.buf(3)
+            dw = ops.combine_bwd_p2p(dout, sym.peers(1), sym.peers(2), plan.dest_rank,
+                                     plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
+            sym.barrier()
         else:
             send_sizes, recv_counts, max_seg = sizes
             dret = torch.empty_like(ret)
@@ -225,12 +271,12 @@ class _MoEFunction(torch.autograd.Function):
             stage = torch.empty((sum(recv_counts), d), dtype=torch.bfloat16, device=dev)
             comm.all_to_all_rows(stage, dret, recv_counts, send_sizes, group)
             dY = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
+            dX = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
             ops.zero_pad_rows(dY, plan.recv_m, plan.recv_off)
             ops.copy_segments(stage, dY, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
                               max_seg)
             del dret, stage
         dH = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=dev)
-        dX = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
         dW1 = torch.empty_like(w1)
         dW2 = torch.empty_like(w2)
         if G > 0:
@@ -242,8 +288,12 @@ class _MoEFunction(torch.autograd.Function):
             # variable-K weight gradients: dW1_e = dH_e^T X_e, dW2_e = dY_e^T A_e
             ops.grouped_gemm_wgrad(dH, X, off, dW1)
             ops.grouped_gemm_wgrad(dY, A, off, dW2)
-        if N == 1:
-            dxe, drow = dX, row
+        if mode == "local":
+            dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
+        elif mode == "p2p":
+            sym.barrier()
+            dx, dlog = ops.dispatch_bwd_p2p(sym.peers(3), plan.dest_rank, plan.dest_row, probs,
+                                            idx, dw, wg, layer.renorm, Tn, d)
         else:
             send_sizes, recv_counts, max_seg = sizes
             dXst = torch.empty((sum(recv_counts), d), dtype=torch.bfloat16, device=dev)
@@ -251,8 +301,7 @@ class _MoEFunction(torch.autograd.Function):
                               max_seg)
             dxe = torch.empty((Tn * k, d), dtype=torch.bfloat16, device=dev)
             comm.all_to_all_rows(dxe, dXst, send_sizes, recv_counts, group)
-            drow = row
-        dx, dlog = ops.dispatch_bwd(dxe, drow, probs, idx, dw, wg, layer.renorm, Tn)
+            dx, dlog = ops.dispatch_bwd(dxe, row, probs, idx, dw, wg, layer.renorm, Tn)
         dwg, dbg = ops.router_wgrad(dlog, x)
         if N > 1:
             layer.replica_groups.allreduce([dW1, dW2], layer.local_ids)

@@ -162,3 +162,42 @@ def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0):
     _gemm(1, ptr(A), ptr(B), ptr(C), None, G, ptr(off), rows, M, N, 0, _lib.LZ_MN_MAJOR,
           _lib.LZ_EPI_STORE, num_sms, _s())
     return C
+
+
+# ------------------------------------------------- fused exchange over NVLink peers
+
+def pack_p2p(x, dest_rank, dest_row, k: int, peers, own, recv_m, recv_off):
+    """x rows -> their destination rank's symmetric receive buffer (P2P stores)."""
+    Tn, d = x.shape
+    _lib.call("lz_pack_p2p", ptr(x), Tn, d, k, ptr(dest_rank), ptr(dest_row), ptr(peers),
+              ptr(own), recv_m.numel(), ptr(recv_m), ptr(recv_off), _s())
+
+
+def combine_p2p(peers_y, dest_rank, dest_row, w, k: int, d: int, out=None):
+    Tn = w.shape[0]
+    if out is None:
+        out = torch.empty((Tn, d), dtype=torch.bfloat16, device=w.device)
+    _lib.call("lz_combine_p2p", ptr(peers_y), ptr(dest_rank), ptr(dest_row), ptr(w), Tn, d, k,
+              ptr(out), _s())
+    return out
+
+
+def combine_bwd_p2p(dout, peers_y, peers_dy, dest_rank, dest_row, w, k: int, own_dy, recv_m,
+                    recv_off):
+    Tn, d = dout.shape
+    dw = torch.empty((Tn, k), dtype=torch.float32, device=dout.device)
+    _lib.call("lz_combine_bwd_p2p", ptr(dout), ptr(peers_y), ptr(peers_dy), ptr(dest_rank),
+              ptr(dest_row), ptr(w), Tn, d, k, ptr(dw), ptr(own_dy), recv_m.numel(), ptr(recv_m),
+              ptr(recv_off), _s())
+    return dw
+
+
+def dispatch_bwd_p2p(peers_dxe, dest_rank, dest_row, probs, idx, dw, wg, renorm: bool, Tn: int,
+                     d: int):
+    k = idx.shape[1]
+    E = probs.shape[1]
+    dx = torch.empty((Tn, d), dtype=torch.bfloat16, device=probs.device)
+    dlog = torch.empty((Tn, E), dtype=torch.float32, device=probs.device)
+    _lib.call("lz_dispatch_bwd_p2p", ptr(peers_dxe), ptr(dest_rank), ptr(dest_row), Tn, d, k,
+              ptr(probs), ptr(idx), ptr(dw), ptr(wg), E, int(renorm), ptr(dx), ptr(dlog), _s())
+    return dx, dlog
