@@ -72,6 +72,7 @@ class MoELayer(torch.nn.Module):
         self._symm = None
         self._symm_group = None
         self._fwd_version = 0
+        self.stage_events: list | None = None
         self.set_plan(replicas)
 
     # ------------------------------------------------------------- plan
@@ -155,6 +156,24 @@ class MoELayer(torch.nn.Module):
         return float(recv.max() / recv.mean().clamp_min(1))
 
 
+def _mark(layer, name: str) -> None:
+    """Stage timing (bench --breakdown): CUDA event on the current stream."""
+    if layer.stage_events is not None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        layer.stage_events.append((name, e))
+
+
+def stage_breakdown(events) -> dict:
+    """{stage: ms} from consecutive marks (a stage = time since the previous mark)."""
+    out: dict = {}
+    for (_, a), (name, b) in zip(events, events[1:]):
+        if name in ("fwd_start", "bwd_start"):
+            continue
+        out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+    return out
+
+
 def _capacity(rows: int) -> int:
     return (rows + ALIGN - 1) // ALIGN * ALIGN
 
@@ -169,11 +188,15 @@ class _MoEFunction(torch.autograd.Function):
         k, E, G = layer.k, layer.E, len(layer.local_ids)
         N, rank, group = layer.world, layer.rank, layer.group
         mode = layer.exchange_mode()
+        _mark(layer, "fwd_start")
         idx, w, probs, hist = ops.router_gate(x, wg, bg, k, layer.renorm)
+        _mark(layer, "gate")
         T = comm.allgather_hist(hist, group)
+        _mark(layer, "hist_allgather")
         plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ALIGN)
         layer.last_plan = plan
         off = plan.recv_off.index_select(0, layer._off_index).contiguous()
+        _mark(layer, "plan")
         P = Tn * k
         sizes = None
         if mode == "local":
@@ -212,12 +235,14 @@ class _MoEFunction(torch.autograd.Function):
             ops.copy_segments(stage, X, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
                               max_seg)
             del send, stage
+        _mark(layer, "dispatch")
         d_ff = layer.d_ff
         H = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
         A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
         if G > 0:
             ops.grouped_gemm_rows(X, w1, off, A, epilogue=_lib.LZ_EPI_GELU, aux=H)
             ops.grouped_gemm_rows(A, w2, off, Y)
+        _mark(layer, "ffn_fwd")
         if mode == "local":
             out = ops.combine(Y, plan.dest_row, w, k)
             ret, row = Y, plan.dest_row
@@ -234,6 +259,7 @@ class _MoEFunction(torch.autograd.Function):
             comm.all_to_all_rows(ret, Yst, send_sizes, recv_counts, group)
             out = ops.combine(ret, plan.slot, w, k)
             row = plan.slot
+        _mark(layer, "combine")
         ctx.layer = layer
         ctx.meta = (Tn, cap, sizes, mode, layer._fwd_version)
         ctx.plan = plan
@@ -250,6 +276,7 @@ class _MoEFunction(torch.autograd.Function):
         d, d_ff = layer.d, layer.d_ff
         G = len(layer.local_ids)
         dout = dout.contiguous().to(torch.bfloat16)
+        _mark(layer, "bwd_start")
         dev = x.device
         if mode == "local":
             dY = torch.empty((cap, d), dtype=torch.bfloat16, device=dev)
@@ -276,6 +303,7 @@ class _MoEFunction(torch.autograd.Function):
             ops.copy_segments(stage, dY, plan.recv_stage_off, plan.recv_src_off, plan.recv_cnt,
                               max_seg)
             del dret, stage
+        _mark(layer, "combine_bwd")
         dH = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=dev)
         dW1 = torch.empty_like(w1)
         dW2 = torch.empty_like(w2)
@@ -288,6 +316,7 @@ class _MoEFunction(torch.autograd.Function):
             # variable-K weight gradients: dW1_e = dH_e^T X_e, dW2_e = dY_e^T A_e
             ops.grouped_gemm_wgrad(dH, X, off, dW1)
             ops.grouped_gemm_wgrad(dY, A, off, dW2)
+        _mark(layer, "ffn_bwd")
         if mode == "local":
             dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
         elif mode == "p2p":
@@ -302,13 +331,16 @@ class _MoEFunction(torch.autograd.Function):
             dxe = torch.empty((Tn * k, d), dtype=torch.bfloat16, device=dev)
             comm.all_to_all_rows(dxe, dXst, send_sizes, recv_counts, group)
             dx, dlog = ops.dispatch_bwd(dxe, row, probs, idx, dw, wg, layer.renorm, Tn)
+        _mark(layer, "dispatch_bwd")
         dwg, dbg = ops.router_wgrad(dlog, x)
+        _mark(layer, "router_wgrad")
         if N > 1:
             layer.replica_groups.allreduce([dW1, dW2], layer.local_ids)
             flat = torch.cat([dwg.view(-1), dbg])
             dist.all_reduce(flat, group=group)
             dwg = flat[:dwg.numel()].view_as(dwg)
             dbg = flat[dwg.numel():]
+        _mark(layer, "grad_sync")
         return dx, dwg.to(wg.dtype), dbg, dW1, dW2, None
 
 
