@@ -197,11 +197,15 @@ lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, in
  *                      A K-major [rows, K]; B_g = B[g*N:(g+1)*N, :K] (b_major = K) or
  *                      B[g*K:(g+1)*K, :N] (b_major = MN)
  *   mode 1 ("wgrad"):  C_g[M, N] = A[off[g]:off[g+1], :M]^T . B[off[g]:off[g+1], :N]
- *                      (both MN-major, variable K = segment length, C at C + g*M*N)
- * M, N, K multiples of 128 / 256 / 64 as documented in DESIGN.md. */
+ *                      (both MN-major, variable K = segment length); C_g starts at row
+ *                      g*c_group_rows + c_row_offset of C viewed as [*, N] (c_group_rows = 0
+ *                      means M: dense [G, M, N]); lets dW1/dW2 interleave in one flat
+ *                      per-expert gradient buffer that is all-reduced without copies
+ * M, N, K multiples of 128 / 256 / 64; G <= 128. */
 lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux, int G,
                           const int32_t* off, int rows_total, int M, int N, int K, int b_major,
-                          int epilogue, int num_sms, void* stream);
+                          int epilogue, int num_sms, int c_group_rows, int c_row_offset,
+                          void* stream);
 
 #ifdef __cplusplus
 }

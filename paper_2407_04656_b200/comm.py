@@ -117,11 +117,12 @@ class ReplicaGroups:
         if self.n == 1:
             return
         for pg, pos in self.buckets(local_ids):
-            idx = torch.tensor(pos, device=grads[0].device)
-            flat = torch.cat([g.index_select(0, idx).reshape(-1) for g in grads])
-            dist.all_reduce(flat, group=pg)
-            o = 0
+            # maximal runs of consecutive local positions: in-place views, no copies
+            runs, a = [], pos[0]
+            for x, y in zip(pos, pos[1:] + [None]):
+                if y != x + 1:
+                    runs.append((a, x + 1))
+                    a = y
             for g in grads:
-                n = g[0].numel() * len(pos)
-                g.index_copy_(0, idx, flat[o:o + n].view(len(pos), *g.shape[1:]))
-                o += n
+                for a, b in runs:
+                    dist.all_reduce(g[a:b], group=pg)

@@ -189,6 +189,8 @@ __device__ __forceinline__ float dgelu_f(float x) {
 
 struct Params {
   int mode;         // 0 rows, 1 wgrad
+  int c_grp_rows;   // mode 1: rows between consecutive groups' C blocks (>= M)
+  int c_row_off;    // mode 1: row offset of group 0's C block
   int G;            // groups
   int M, N, K;      // mode 0: N, K used; mode 1: M, N
   const int32_t* off;
@@ -386,7 +388,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
       const TileInfo t = decode_tile(p, s_pref, s_off, tile);
-      const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.M) + t.mb * BM + quad * 32;
+      const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
+                       t.mb * BM + quad * 32;
       const int col0 = t.nb * BN;
       if (dgelu && lane == 0) {
         // prefetch the first two pre-activation chunks of this tile
@@ -530,7 +533,7 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
 extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
                                      int G, const int32_t* off, int rows_total, int M, int N,
                                      int K, int b_major, int epilogue, int num_sms,
-                                     void* stream) {
+                                     int c_group_rows, int c_row_offset, void* stream) {
   if (G < 1 || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
   if (G > kMaxGroups) return LZ_ERR_UNSUPPORTED;
   if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DGELU) return LZ_ERR_ARG;
@@ -545,6 +548,8 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.K = K;
   p.off = off;
   p.epilogue = epilogue;
+  p.c_grp_rows = c_group_rows > 0 ? c_group_rows : M;
+  p.c_row_off = c_row_offset;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (rows_total == 0 && mode == 0) return LZ_OK;
@@ -569,7 +574,11 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
     const uint64_t rows = rows_total > 0 ? rows_total : 1;
     if (!make_map(&ma, A, M, rows, 64, BK)) return LZ_ERR_CUDA;
     if (!make_map(&mb, B, N, rows, 64, BK)) return LZ_ERR_CUDA;
-    if (!make_map(&mc, C, N, (uint64_t)G * M, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
+    if (c_group_rows != 0 && (c_group_rows < M || c_row_offset < 0 ||
+                              c_row_offset + M > c_group_rows))
+      return LZ_ERR_ARG;
+    const uint64_t c_rows = (uint64_t)(G - 1) * p.c_grp_rows + c_row_offset + M;
+    if (!make_map(&mc, C, N, c_rows, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     long tiles = (long)G * (M / BM) * (N / BN);
     int grid = (int)(tiles < sms ? tiles : sms);
     return launch<1, 1>(ma, mb, mc, mc, p, grid, s);

@@ -149,18 +149,21 @@ def grouped_gemm_rows(A, B, off, C, *, b_major=_lib.LZ_K_MAJOR, epilogue=_lib.LZ
     G = off.numel() - 1
     N = B.shape[1] if b_major == _lib.LZ_K_MAJOR else B.shape[2]
     _gemm(0, ptr(A), ptr(B), ptr(C), ptr(aux), G, ptr(off), rows, 0, N, K, b_major, epilogue,
-          num_sms, _s())
+          num_sms, 0, 0, _s())
     return C
 
 
-def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0):
-    """C[g] = A[off[g]:off[g+1]]^T . B[off[g]:off[g+1]]; A [rows, M], B [rows, N], C [G, M, N]."""
+def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0, c_group_rows: int = 0,
+                       c_row_offset: int = 0):
+    """C_g = A[off[g]:off[g+1]]^T . B[off[g]:off[g+1]]; A [rows, M], B [rows, N].
+    C is [G, M, N] (default) or any buffer where C_g starts at row g*c_group_rows +
+    c_row_offset of C viewed as [*, N]."""
     _cuda(A, B, off, C)
     rows, M = A.shape
     N = B.shape[1]
     G = off.numel() - 1
     _gemm(1, ptr(A), ptr(B), ptr(C), None, G, ptr(off), rows, M, N, 0, _lib.LZ_MN_MAJOR,
-          _lib.LZ_EPI_STORE, num_sms, _s())
+          _lib.LZ_EPI_STORE, num_sms, c_group_rows, c_row_offset, _s())
     return C
 
 

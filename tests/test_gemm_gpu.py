@@ -118,3 +118,19 @@ def test_persistent_grid_smaller_than_tiles():
     torch.cuda.synchronize()
     for g in range(2):
         _close(C[off[g]:off[g + 1]], A[off[g]:off[g + 1]].float() @ B[g].float().t())
+
+
+def test_wgrad_interleaved_output():
+    """c_group_rows / c_row_offset place C_g inside a flat per-expert buffer."""
+    torch.manual_seed(5)
+    off_t, off = _offsets([128, 256])
+    M, N = 256, 512
+    A = torch.randn(off[-1], M, device="cuda").bfloat16()
+    B = torch.randn(off[-1], N, device="cuda").bfloat16()
+    buf = torch.zeros(2, 3 * M, N, device="cuda").bfloat16()   # per group: [pad M | C_g | pad M]
+    ops.grouped_gemm_wgrad(A, B, off_t, buf, c_group_rows=3 * M, c_row_offset=M)
+    torch.cuda.synchronize()
+    for g in range(2):
+        sl = slice(off[g], off[g + 1])
+        _close(buf[g, M:2 * M], A[sl].float().t() @ B[sl].float())
+        assert (buf[g, :M] == 0).all() and (buf[g, 2 * M:] == 0).all()
