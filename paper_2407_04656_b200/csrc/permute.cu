@@ -179,100 +179,110 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
   }
 }
 
-// Gate backward (softmax + top-k (+renorm)) and dispatch backward, one warp per token.
+// Gate backward (softmax + top-k (+renorm)) and dispatch backward.  A warp owns a
+// group of kTG tokens: it first computes their dlogits (lane = expert), then sweeps the
+// row in 16-byte chunks accumulating sum_s dxe[row(t,s)] + dlogits[t,:] . wg for all kTG
+// tokens at once, so each wg chunk is read from L1 once per kTG tokens.
+constexpr int kTG = 8;
 __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
     const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
     int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
     const float* __restrict__ dwv, const uint4* __restrict__ wg, int E, int renorm,
     uint4* __restrict__ dx, float* __restrict__ dlogits) {
-  const int lane = threadIdx.x % 32;
-  const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
+  __shared__ float s_dl[kRowWarps][kTG][64];
+  __shared__ long long s_src[kRowWarps][kTG][LZ_MAX_TOPK];  // row base address per (token, s)
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const long gw = (long)blockIdx.x * kRowWarps + warp;
   const long nw = (long)gridDim.x * kRowWarps;
   const int nch = d / 8;
-  for (long t = gw; t < Tn; t += nw) {
-    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
-    const int my_idx = lane < k ? __ldg(idx + t * k + lane) : -1;
-    const float my_dw = lane < k ? __ldg(dwv + t * k + lane) : 0.f;
-    const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
-    // lane owns experts e = lane and e = lane + 32 (E <= 64)
-    float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int e = lane + 32 * h;
-      if (e < E) p[h] = __ldg(probs + t * E + e);
-    }
-    // top-k probs and S for renorm
-    float S = 0.f, sum_dw_w = 0.f;
-    if (renorm) {
-      for (int s = 0; s < k; ++s) {
-        const int es = __shfl_sync(0xffffffffu, my_idx, s);
-        const float ps = __ldg(probs + t * E + es);
-        S += ps;
+  for (long t0 = gw * kTG; t0 < Tn; t0 += nw * kTG) {
+    for (int ti = 0; ti < kTG; ++ti) {
+      const long t = t0 + ti;
+      if (t >= Tn) {
+        s_dl[warp][ti][lane] = 0.f;
+        s_dl[warp][ti][lane + 32] = 0.f;
+        continue;
       }
-      for (int s = 0; s < k; ++s) {
-        const int es = __shfl_sync(0xffffffffu, my_idx, s);
-        const float dws = __shfl_sync(0xffffffffu, my_dw, s);
-        sum_dw_w += dws * (__ldg(probs + t * E + es) / S);
+      const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+      const int my_idx = lane < k ? __ldg(idx + t * k + lane) : -1;
+      const float my_dw = lane < k ? __ldg(dwv + t * k + lane) : 0.f;
+      const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
+      if (lane < k) {
+        const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[my_rk]) : dxe;
+        s_src[warp][ti][lane] = (long long)(base + (long)my_row * nch);
+      }
+      // lane owns experts e = lane and e = lane + 32 (E <= 64)
+      float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        if (e < E) p[h] = __ldg(probs + t * E + e);
+      }
+      float S = 0.f, sum_dw_w = 0.f;
+      if (renorm) {
+        for (int s2 = 0; s2 < k; ++s2) {
+          const int es = __shfl_sync(0xffffffffu, my_idx, s2);
+          S += __ldg(probs + t * E + es);
+        }
+        for (int s2 = 0; s2 < k; ++s2) {
+          const int es = __shfl_sync(0xffffffffu, my_idx, s2);
+          const float dws = __shfl_sync(0xffffffffu, my_dw, s2);
+          sum_dw_w += dws * (__ldg(probs + t * E + es) / S);
+        }
+      }
+      for (int s2 = 0; s2 < k; ++s2) {
+        const int es = __shfl_sync(0xffffffffu, my_idx, s2);
+        const float dws = __shfl_sync(0xffffffffu, my_dw, s2);
+        const float g = renorm ? (dws - sum_dw_w) / S : dws;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (es == lane + 32 * h) dp[h] += g;
+      }
+      const float pdp = warp_sum(p[0] * dp[0] + p[1] * dp[1]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = lane + 32 * h;
+        const float dl = p[h] * (dp[h] - pdp);
+        s_dl[warp][ti][e] = dl;
+        if (e < E) dlogits[t * E + e] = dl;
       }
     }
-    for (int s = 0; s < k; ++s) {
-      const int es = __shfl_sync(0xffffffffu, my_idx, s);
-      const float dws = __shfl_sync(0xffffffffu, my_dw, s);
-      const float g = renorm ? (dws - sum_dw_w) / S : dws;
+    __syncwarp();
+    const int nt = (int)min((long)kTG, Tn - t0);
+    for (int c = lane; c < nch; c += 32) {
+      float acc[kTG][8];
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
-        if (es == lane + 32 * h) dp[h] += g;
-    }
-    const float pdp = warp_sum(p[0] * dp[0] + p[1] * dp[1]);
-    float dl[2];
+      for (int ti = 0; ti < kTG; ++ti) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int e = lane + 32 * h;
-      dl[h] = p[h] * (dp[h] - pdp);
-      if (e < E) dlogits[t * E + e] = dl[h];
-    }
-    for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
-      float acc[kVec][8];
-#pragma unroll
-      for (int u = 0; u < kVec; ++u)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[u][q] = 0.f;
-      for (int s = 0; s < k; ++s) {
-        const long r = __shfl_sync(0xffffffffu, my_row, s);
-        const uint4* src = row_base(const_cast<uint4*>(dxe), peers, my_rk, s) + r * nch;
-        uint4 v[kVec];
-#pragma unroll
-        for (int u = 0; u < kVec; ++u)
-          if (c0 + 32 * u < nch) v[u] = ld_nc_v4(src + c0 + 32 * u);
-#pragma unroll
-        for (int u = 0; u < kVec; ++u) {
-          if (c0 + 32 * u < nch) {
+        for (int q = 0; q < 8; ++q) acc[ti][q] = 0.f;
+        if (ti < nt) {
+          for (int s2 = 0; s2 < k; ++s2) {
+            const uint4* src = reinterpret_cast<const uint4*>(s_src[warp][ti][s2]);
             float f[8];
-            bf16x8_to_f32(v[u], f);
+            bf16x8_to_f32(ld_nc_v4(src + c), f);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[u][q] += f[q];
+            for (int q = 0; q < 8; ++q) acc[ti][q] += f[q];
           }
         }
       }
       if (wg) {
         for (int e = 0; e < E; ++e) {
-          const float de = __shfl_sync(0xffffffffu, dl[e >> 5], e & 31);
+          float f[8];
+          bf16x8_to_f32(__ldg(wg + (long)e * nch + c), f);
 #pragma unroll
-          for (int u = 0; u < kVec; ++u) {
-            if (c0 + 32 * u < nch) {
-              float f[8];
-              bf16x8_to_f32(__ldg(wg + (long)e * nch + c0 + 32 * u), f);
+          for (int ti = 0; ti < kTG; ++ti) {
+            const float de = s_dl[warp][ti][e];
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc[u][q] = fmaf(de, f[q], acc[u][q]);
-            }
+            for (int q = 0; q < 8; ++q) acc[ti][q] = fmaf(de, f[q], acc[ti][q]);
           }
         }
       }
 #pragma unroll
-      for (int u = 0; u < kVec; ++u)
-        if (c0 + 32 * u < nch) st_v4(dx + t * nch + c0 + 32 * u, f32_to_bf16x8(acc[u]));
+      for (int ti = 0; ti < kTG; ++ti)
+        if (ti < nt) st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(acc[ti]));
     }
+    __syncwarp();
   }
 }
 
@@ -280,7 +290,7 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
 // [by*1024, +1024) and experts [bz*16, +16); thread owns 4 columns x 16 experts.
 constexpr int kWgE = 16;
 constexpr int kWgTokTile = 64;
-__global__ void __launch_bounds__(256) router_wgrad_partial(const float* __restrict__ dlog,
+__global__ void __launch_bounds__(256, 2) router_wgrad_partial(const float* __restrict__ dlog,
                                                             const __nv_bfloat16* __restrict__ x,
                                                             int Tn, int d, int E,
                                                             float* __restrict__ part,
@@ -310,7 +320,29 @@ __global__ void __launch_bounds__(256) router_wgrad_partial(const float* __restr
     if (blockIdx.y == 0 && threadIdx.x < kWgE)
       for (int ti = 0; ti < nt; ++ti) bacc += s_dl[ti][threadIdx.x];
     if (col < d) {
-      for (int ti = 0; ti < nt; ++ti) {
+      int ti = 0;
+      for (; ti + 8 <= nt; ti += 8) {
+        uint2 raw[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          raw[u] = __ldg(reinterpret_cast<const uint2*>(x + (tt + ti + u) * d + col));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float x0 = __uint_as_float(raw[u].x << 16);
+          const float x1 = __uint_as_float(raw[u].x & 0xffff0000u);
+          const float x2 = __uint_as_float(raw[u].y << 16);
+          const float x3 = __uint_as_float(raw[u].y & 0xffff0000u);
+#pragma unroll
+          for (int e = 0; e < kWgE; ++e) {
+            const float g = s_dl[ti + u][e];
+            acc[e][0] = fmaf(g, x0, acc[e][0]);
+            acc[e][1] = fmaf(g, x1, acc[e][1]);
+            acc[e][2] = fmaf(g, x2, acc[e][2]);
+            acc[e][3] = fmaf(g, x3, acc[e][3]);
+          }
+        }
+      }
+      for (; ti < nt; ++ti) {
         const uint2 raw = __ldg(reinterpret_cast<const uint2*>(x + (tt + ti) * d + col));
         const float x0 = __uint_as_float(raw.x << 16), x1 = __uint_as_float(raw.x & 0xffff0000u);
         const float x2 = __uint_as_float(raw.y << 16), x3 = __uint_as_float(raw.y & 0xffff0000u);
@@ -486,7 +518,7 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
     return LZ_ERR_ARG;
   if (Tn == 0) return LZ_OK;
   if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
-  dispatch_bwd_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
+  dispatch_bwd_kernel<<<row_grid((Tn + kTG - 1) / kTG), kRowThreads, 0, (cudaStream_t)stream>>>(
       (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const uint4*)wg, E, renorm,
       (uint4*)dx, dlogits);
   return lzh::check_launch();
@@ -512,7 +544,7 @@ extern "C" lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe,
 }
 
 static int wgrad_nblk(int Tn) {
-  int n = lzh::num_sms();
+  int n = 2 * lzh::num_sms();
   long per = (Tn + n - 1) / n;
   if (per < 64) n = (Tn + 63) / 64;
   return n < 1 ? 1 : n;
