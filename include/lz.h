@@ -201,11 +201,18 @@ lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, in
  *                      g*c_group_rows + c_row_offset of C viewed as [*, N] (c_group_rows = 0
  *                      means M: dense [G, M, N]); lets dW1/dW2 interleave in one flat
  *                      per-expert gradient buffer that is all-reduced without copies
- * M, N, K multiples of 128 / 256 / 64; G <= 128. */
+ * M, N, K multiples of lz_gemm_row_align() / 256 / 64; mode-0 segments multiples of
+ * lz_gemm_row_align(); mode-1 segments multiples of 64; G <= 128. */
 lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux, int G,
                           const int32_t* off, int rows_total, int M, int N, int K, int b_major,
                           int epilogue, int num_sms, int c_group_rows, int c_row_offset,
                           void* stream);
+
+/* GEMM variant: 2 = CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles; default),
+ * 1 = single-CTA kernel (128-row tiles).  Returns the active value. */
+int lz_gemm_set_cta_group(int cta_group);
+/* Row alignment mode-0 group segments must have for the active variant (128 or 256). */
+int lz_gemm_row_align(void);
 
 #ifdef __cplusplus
 }

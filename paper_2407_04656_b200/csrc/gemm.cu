@@ -18,12 +18,8 @@
 namespace lz {
 namespace gemm {
 
-constexpr int BM = 128, BN = 256, BK = 64;
-constexpr int kStages = 4;
+constexpr int BM = 128, BN = 256, BK = 64;  // per-CTA rows, tile columns, k block
 constexpr int kThreads = 192;
-constexpr int kATileBytes = BM * BK * 2;  // 16 KB
-constexpr int kBTileBytes = BN * BK * 2;  // 32 KB
-constexpr int kStageBytes = kATileBytes + kBTileBytes;
 constexpr int kAccCols = BN;              // fp32 accumulator columns per buffer
 constexpr int kTmemCols = 2 * kAccCols;   // 512
 constexpr int kMaxGroups = 128;
@@ -34,11 +30,25 @@ constexpr int kEpiCols = 32;
 constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
 constexpr int kEpiWarpBytes = 4 * kEpiBuf;          // out0 out1 aux0 aux1
 constexpr int kEpiBytes = 4 * kEpiWarpBytes;        // 32 KB
-constexpr int kTilesBytes = kStages * kStageBytes;  // 192 KB
 constexpr int kBarBytes = 256;
 constexpr int kTabBytes = 2 * (kMaxGroups + 1) * 4;
-constexpr int kSmemBytes = 1024 /*align slack*/ + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
-static_assert(kSmemBytes <= 232448, "shared memory budget");
+
+// CG = 1: one CTA per 128 x 256 tile (UMMA 128x256x16, cta_group::1), 4 stages x 48 KB.
+// CG = 2: a CTA pair per 256 x 256 tile (UMMA 256x256x16, cta_group::2): each CTA stages
+//         its 128 rows of A and half (128 columns) of B -> 32 KB/stage, 6 stages; the
+//         leader CTA issues the MMAs for both, halving per-SM smem operand traffic.
+template <int CG>
+struct Cfg {
+  static constexpr int kBRows = BN / CG;                 // B rows (n) staged per CTA
+  static constexpr int kATileBytes = BM * BK * 2;        // 16 KB
+  static constexpr int kBTileBytes = kBRows * BK * 2;    // 32 KB / 16 KB
+  static constexpr int kStageBytes = kATileBytes + kBTileBytes;
+  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kTilesBytes = kStages * kStageBytes;
+  static constexpr int kTileM = BM * CG;                 // rows per (pair) tile
+  static constexpr int kSmemBytes = 1024 + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
+  static_assert(kSmemBytes <= 232448, "shared memory budget");
+};
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -82,6 +92,73 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// 2-CTA variant: the transaction bytes are credited to the leader CTA's barrier (the
+// CTA-rank bit 24 of the shared::cluster address cleared), data lands in local smem.
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tma_load(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                         int c1) {
+  if (CG == 1) tma_load_2d(dst, map, bar, c0, c1);
+  else tma_load_2d_cg2(dst, map, bar, c0, c1);
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "r"(cta)
+      : "memory");
+}
+template <int CG>
+__device__ __forceinline__ void tc_commit_cg(uint64_t* bar) {
+  if (CG == 1) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+  } else {
+    // arrive on the same barrier in both CTAs of the pair
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tc_mma_cg(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accum) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
                                              int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -150,9 +227,9 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N>>3, M>>4.
-__host__ __device__ constexpr uint32_t make_idesc(int a_mn, int b_mn) {
+__host__ __device__ constexpr uint32_t make_idesc(int a_mn, int b_mn, int m = BM) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
-         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
@@ -198,25 +275,25 @@ struct Params {
 };
 
 // A tile load (128 x 64) for the current stage
-template <int A_MN>
+template <int A_MN, int CG>
 __device__ __forceinline__ void load_a(const CUtensorMap* map, uint8_t* dst, uint64_t* bar,
                                        int row_or_k, int m0, int k0) {
   if (A_MN == 0) {
-    tma_load_2d(dst, map, bar, k0, row_or_k);  // K-major: (k, row)
+    tma_load<CG>(dst, map, bar, k0, row_or_k);  // K-major: (k, row), 128 rows
   } else {
     // MN-major: two 64-wide M boxes of 64 k-rows
-    tma_load_2d(dst, map, bar, m0, row_or_k);
-    tma_load_2d(dst + 8192, map, bar, m0 + 64, row_or_k);
+    tma_load<CG>(dst, map, bar, m0, row_or_k);
+    tma_load<CG>(dst + 8192, map, bar, m0 + 64, row_or_k);
   }
 }
-template <int B_MN>
+template <int B_MN, int CG>
 __device__ __forceinline__ void load_b(const CUtensorMap* map, uint8_t* dst, uint64_t* bar,
                                        int n_row, int n0, int k_row, int k0) {
   if (B_MN == 0) {
-    tma_load_2d(dst, map, bar, k0, n_row);  // K-major (k, n-row)
+    tma_load<CG>(dst, map, bar, k0, n_row);  // K-major (k, n-row), BN/CG rows
   } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tma_load_2d(dst + 8192 * q, map, bar, n0 + 64 * q, k_row);
+    for (int q = 0; q < 4 / CG; ++q) tma_load<CG>(dst + 8192 * q, map, bar, n0 + 64 * q, k_row);
   }
 }
 
@@ -224,8 +301,10 @@ struct TileInfo {
   int g, mb, nb, nk;
 };
 
+template <int CG>
 __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
                                                 const int32_t* s_off, int tile) {
+  // (tiles are TileM x BN; mb counts TileM blocks)
   // binary search the group: s_pref[g] <= tile < s_pref[g+1]
   int lo = 0, hi = p.G - 1;
   while (lo < hi) {
@@ -243,19 +322,20 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
   return t;
 }
 
-template <int A_MN, int B_MN>
+template <int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
                         const __grid_constant__ CUtensorMap map_x, const Params p) {
+  using C = Cfg<CG>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* s_tiles = smem;
-  uint8_t* s_epi = smem + kTilesBytes;
+  uint8_t* s_epi = smem + C::kTilesBytes;
   uint64_t* full_bar = (uint64_t*)(s_epi + kEpiBytes);
-  uint64_t* empty_bar = full_bar + kStages;
-  uint64_t* tfull_bar = empty_bar + kStages;
+  uint64_t* empty_bar = full_bar + C::kStages;
+  uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint64_t* aux_bar = tempty_bar + 2;  // [4 warps][2 buffers]
   uint32_t* s_tmem = (uint32_t*)(aux_bar + 8);
@@ -263,6 +343,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t cta = CG == 1 ? 0u : cluster_ctarank();
+  const bool leader = cta == 0;
+  const int unit = CG == 1 ? blockIdx.x : (blockIdx.x >> 1);   // tile-processing unit
+  const int nunits = CG == 1 ? gridDim.x : (gridDim.x >> 1);
 
   // group table -> tile prefix (every CTA computes it; G <= kMaxGroups)
   for (int g = threadIdx.x; g <= p.G; g += blockDim.x) s_off[g] = p.off[g];
@@ -272,18 +356,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nbn = p.N / BN;
     for (int g = 0; g < p.G; ++g) {
       s_pref[g] = acc;
-      acc += (p.mode == 0) ? ((s_off[g + 1] - s_off[g]) / BM) * nbn : (p.M / BM) * nbn;
+      acc += (p.mode == 0) ? ((s_off[g + 1] - s_off[g]) / C::kTileM) * nbn
+                           : (p.M / C::kTileM) * nbn;
     }
     s_pref[p.G] = acc;
   }
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < C::kStages; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 128);
+      mbar_init(&tempty_bar[s], 4 * CG);  // one arrival per epilogue warp of each CTA
     }
     for (int s = 0; s < 8; ++s) mbar_init(&aux_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -293,40 +378,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (p.epilogue != LZ_EPI_STORE) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(s_tmem)),
-                 "r"(kTmemCols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 1) __syncthreads();
+  else cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
   const int total = s_pref[p.G];
 
   if (warp == 0) {
     if (lane == 0) {
-      // ===== TMA producer =====
+      // ===== TMA producer (both CTAs of a pair load their halves) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+      for (int tile = unit; tile < total; tile += nunits) {
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
         for (int kb = 0; kb < t.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sa = s_tiles + stage * kStageBytes;
-          uint8_t* sb = sa + kATileBytes;
-          mbar_expect_tx(&full_bar[stage], kStageBytes);
+          uint8_t* sa = s_tiles + stage * C::kStageBytes;
+          uint8_t* sb = sa + C::kATileBytes;
+          if (leader) mbar_expect_tx(&full_bar[stage], CG * C::kStageBytes);
           if (p.mode == 0) {
-            const int row = s_off[t.g] + t.mb * BM;
-            load_a<A_MN>(&map_a, sa, &full_bar[stage], row, 0, kb * BK);
-            load_b<B_MN>(&map_b, sb, &full_bar[stage], t.g * p.N + t.nb * BN, t.nb * BN,
-                         t.g * p.K + kb * BK, kb * BK);
+            const int row = s_off[t.g] + t.mb * C::kTileM + cta * BM;
+            load_a<A_MN, CG>(&map_a, sa, &full_bar[stage], row, 0, kb * BK);
+            load_b<B_MN, CG>(&map_b, sb, &full_bar[stage],
+                             t.g * p.N + t.nb * BN + cta * C::kBRows,
+                             t.nb * BN + cta * C::kBRows, t.g * p.K + kb * BK, kb * BK);
           } else {
             const int krow = s_off[t.g] + kb * BK;
-            load_a<A_MN>(&map_a, sa, &full_bar[stage], krow, t.mb * BM, 0);
-            load_b<B_MN>(&map_b, sb, &full_bar[stage], 0, t.nb * BN, krow, 0);
+            load_a<A_MN, CG>(&map_a, sa, &full_bar[stage], krow, t.mb * C::kTileM + cta * BM, 0);
+            load_b<B_MN, CG>(&map_b, sb, &full_bar[stage], 0, t.nb * BN + cta * C::kBRows, krow,
+                             0);
           }
-          if (++stage == kStages) {
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -334,23 +429,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t idesc = make_idesc(A_MN, B_MN);
+    if (lane == 0 && leader) {
+      // ===== MMA issuer (leader CTA issues for the pair) =====
+      constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BM * CG);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-        const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+      for (int tile = unit; tile < total; tile += nunits) {
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
         for (int kb = 0; kb < t.nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(s_tiles + stage * kStageBytes);
-          const uint32_t sb = sa + kATileBytes;
+          const uint32_t sa = smem_u32(s_tiles + stage * C::kStageBytes);
+          const uint32_t sb = sa + C::kATileBytes;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             // K-major: +32 B per 16-element k step inside the 128 B swizzle atom
@@ -359,15 +454,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                                      : make_desc(sa + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024)
                                      : make_desc(sb + k * 32, 16, 1024);
-            tc_mma(d_tmem, ad, bd, idesc, (kb | k) != 0);
+            tc_mma_cg<CG>(d_tmem, ad, bd, idesc, (kb | k) != 0);
           }
-          tc_commit(&empty_bar[stage]);  // frees the smem slot when these MMAs retire
-          if (++stage == kStages) {
+          tc_commit_cg<CG>(&empty_bar[stage]);  // frees the smem slot(s) when the MMAs retire
+          if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull_bar[acc]);  // accumulator ready for the epilogue
+        tc_commit_cg<CG>(&tfull_bar[acc]);  // accumulator ready for the epilogue(s)
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -386,10 +481,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kChunks = BN / kEpiCols;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
-      const TileInfo t = decode_tile(p, s_pref, s_off, tile);
+    for (int tile = unit; tile < total; tile += nunits) {
+      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
-                       t.mb * BM + quad * 32;
+                       t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN;
       if (dgelu && lane == 0) {
         // prefetch the first two pre-activation chunks of this tile
@@ -413,9 +508,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int q = 0; q < 32; ++q) v[q] = 0u;
         }
         if (c == kChunks - 1) {
-          // accumulator fully read: hand TMEM back to the MMA warp early
+          // accumulator fully read: hand TMEM back to the MMA issuer early
           tc_fence_before();
-          mbar_arrive(&tempty_bar[acc]);
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 1) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_cluster(&tempty_bar[acc], 0);
+          }
         }
         float f[32];
 #pragma unroll
@@ -467,11 +566,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   }
   tc_fence_before();
-  __syncthreads();
+  if (CG == 1) __syncthreads();
+  else cluster_sync_all();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols));
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols));
   }
 }
 
@@ -499,7 +603,7 @@ static EncodeTiledFn get_encoder() {
   return fn;
 }
 
-// 2D bf16 tensor map over a row-major [outer, inner] matrix, 128B swizzle.
+// 2D bf16 tensor map over a row-major [outer, inner] matrix.
 static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                      uint32_t box_inner, uint32_t box_outer,
                      CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
@@ -510,24 +614,57 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
-             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int A_MN, int B_MN>
+static int g_cta_group = 2;  // default: CTA-pair kernel
+
+extern "C" int lz_gemm_set_cta_group(int cg) {
+  if (cg == 1 || cg == 2) g_cta_group = cg;
+  return g_cta_group;
+}
+extern "C" int lz_gemm_row_align(void) { return BM * g_cta_group; }
+
+template <int A_MN, int B_MN, int CG>
 static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN>;
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg<CG>::kSmemBytes) != cudaSuccess)
       return lzh::check_launch();
     attr_set = true;
   }
-  kern<<<grid, kThreads, kSmemBytes, s>>>(ma, mb, mc, mx, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = Cfg<CG>::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, p) != cudaSuccess) return lzh::check_launch();
   return lzh::check_launch();
+}
+
+template <int A_MN, int B_MN>
+static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                           const CUtensorMap& mx, const Params& p, long tiles, int sms,
+                           cudaStream_t s) {
+  if (g_cta_group == 2) {
+    long units = tiles < sms / 2 ? tiles : sms / 2;
+    if (units < 1) units = 1;
+    return launch<A_MN, B_MN, 2>(ma, mb, mc, mx, p, (int)(2 * units), s);
+  }
+  long grid = tiles < sms ? tiles : sms;
+  if (grid < 1) grid = 1;
+  return launch<A_MN, B_MN, 1>(ma, mb, mc, mx, p, (int)grid, s);
 }
 
 extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
@@ -539,6 +676,7 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DGELU) return LZ_ERR_ARG;
   if ((epilogue != LZ_EPI_STORE) && (mode != 0 || !aux)) return LZ_ERR_ARG;
   if (N <= 0 || N % BN) return LZ_ERR_UNSUPPORTED;
+  const int tile_m = BM * g_cta_group;
   CUtensorMap ma, mb, mc, mx;
   Params p{};
   p.mode = mode;
@@ -552,36 +690,36 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.c_row_off = c_row_offset;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
+  if (sms < 2) sms = 2;
   if (rows_total == 0 && mode == 0) return LZ_OK;
   const CUtensorMapSwizzle sw64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  const int brows = BN / g_cta_group;
   if (mode == 0) {
     if (K <= 0 || K % BK) return LZ_ERR_UNSUPPORTED;
     if (!make_map(&ma, A, K, rows_total, BK, BM)) return LZ_ERR_CUDA;
     if (b_major == LZ_K_MAJOR) {
-      if (!make_map(&mb, B, K, (uint64_t)G * N, BK, BN)) return LZ_ERR_CUDA;
+      if (!make_map(&mb, B, K, (uint64_t)G * N, BK, brows)) return LZ_ERR_CUDA;
     } else {
       if (!make_map(&mb, B, N, (uint64_t)G * K, 64, BK)) return LZ_ERR_CUDA;
     }
     if (!make_map(&mc, C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     if (!make_map(&mx, aux ? aux : C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
-    // upper bound of tiles = rows_total/BM * N/BN; the kernel reads the exact count
-    long tiles = (long)(rows_total / BM) * (N / BN);
-    int grid = (int)(tiles < sms ? (tiles > 0 ? tiles : 1) : sms);
-    return b_major == LZ_K_MAJOR ? launch<0, 0>(ma, mb, mc, mx, p, grid, s)
-                                 : launch<0, 1>(ma, mb, mc, mx, p, grid, s);
+    // upper bound of tiles; the kernel reads the exact count from the device offsets
+    long tiles = (long)(rows_total / tile_m) * (N / BN);
+    return b_major == LZ_K_MAJOR ? launch_cg<0, 0>(ma, mb, mc, mx, p, tiles, sms, s)
+                                 : launch_cg<0, 1>(ma, mb, mc, mx, p, tiles, sms, s);
   } else if (mode == 1) {
-    if (M <= 0 || M % BM) return LZ_ERR_UNSUPPORTED;
-    const uint64_t rows = rows_total > 0 ? rows_total : 1;
-    if (!make_map(&ma, A, M, rows, 64, BK)) return LZ_ERR_CUDA;
-    if (!make_map(&mb, B, N, rows, 64, BK)) return LZ_ERR_CUDA;
+    if (M <= 0 || M % tile_m) return LZ_ERR_UNSUPPORTED;
     if (c_group_rows != 0 && (c_group_rows < M || c_row_offset < 0 ||
                               c_row_offset + M > c_group_rows))
       return LZ_ERR_ARG;
+    const uint64_t rows = rows_total > 0 ? rows_total : 1;
+    if (!make_map(&ma, A, M, rows, 64, BK)) return LZ_ERR_CUDA;
+    if (!make_map(&mb, B, N, rows, 64, BK)) return LZ_ERR_CUDA;
     const uint64_t c_rows = (uint64_t)(G - 1) * p.c_grp_rows + c_row_offset + M;
     if (!make_map(&mc, C, N, c_rows, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
-    long tiles = (long)G * (M / BM) * (N / BN);
-    int grid = (int)(tiles < sms ? tiles : sms);
-    return launch<1, 1>(ma, mb, mc, mc, p, grid, s);
+    long tiles = (long)G * (M / tile_m) * (N / BN);
+    return launch_cg<1, 1>(ma, mb, mc, mc, p, tiles, sms, s);
   }
   return LZ_ERR_ARG;
 }

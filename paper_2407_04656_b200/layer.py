@@ -193,7 +193,7 @@ class _MoEFunction(torch.autograd.Function):
         _mark(layer, "gate")
         T = comm.allgather_hist(hist, group)
         _mark(layer, "hist_allgather")
-        plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ALIGN)
+        plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ops.row_align())
         layer.last_plan = plan
         off = plan.recv_off.index_select(0, layer._off_index).contiguous()
         _mark(layer, "plan")

@@ -12,7 +12,16 @@ import torch
 from . import _lib
 from ._lib import ptr
 
-ALIGN = 128  # expert segments of the receive buffer are padded to the GEMM M tile
+ALIGN = 256  # upper bound of the GEMM M tile (receive-buffer expert segments are padded to it)
+
+
+def row_align() -> int:
+    """Padding of expert segments required by the active grouped-GEMM variant."""
+    return int(_lib.raw("lz_gemm_row_align"))
+
+
+def set_gemm_cta_group(cg: int) -> int:
+    return int(_lib.raw("lz_gemm_set_cta_group", cg))
 
 
 def _s():

@@ -13,6 +13,16 @@ pytestmark = pytest.mark.gpu
 from paper_2407_04656_b200 import _lib, ops  # noqa: E402
 
 
+@pytest.fixture(params=[1, 2], ids=["cta1", "cta2"], autouse=True)
+def cg(request):
+    """Run every GEMM test on the single-CTA and on the CTA-pair (cta_group::2) kernel;
+    mode-0 segment sizes are scaled to the variant's row alignment."""
+    prev = ops.set_gemm_cta_group(request.param)
+    yield request.param
+    ops.set_gemm_cta_group(2)
+    del prev
+
+
 def _close(got, ref, rtol=1e-2, atol_scale=1e-2):
     got = got.float()
     ref = ref.float()
@@ -33,9 +43,9 @@ def _offsets(sizes):
 
 @pytest.mark.parametrize("sizes,K,N", [([128], 64, 256), ([128, 256, 0, 384], 128, 256),
                                        ([512, 128], 1024, 512), ([1024], 1024, 4096)])
-def test_rows_kmajor(sizes, K, N):
+def test_rows_kmajor(sizes, K, N, cg):
     torch.manual_seed(0)
-    off_t, off = _offsets(sizes)
+    off_t, off = _offsets([v * cg for v in sizes])
     rows, G = off[-1], len(sizes)
     A = torch.randn(rows, K, device="cuda").bfloat16()
     B = (torch.randn(G, N, K, device="cuda") / K ** 0.5).bfloat16()
@@ -48,9 +58,9 @@ def test_rows_kmajor(sizes, K, N):
 
 
 @pytest.mark.parametrize("sizes,K,N", [([128, 256], 128, 256), ([384, 0, 128], 512, 512)])
-def test_rows_mnmajor_b(sizes, K, N):
+def test_rows_mnmajor_b(sizes, K, N, cg):
     torch.manual_seed(1)
-    off_t, off = _offsets(sizes)
+    off_t, off = _offsets([v * cg for v in sizes])
     rows, G = off[-1], len(sizes)
     A = torch.randn(rows, K, device="cuda").bfloat16()
     B = (torch.randn(G, K, N, device="cuda") / K ** 0.5).bfloat16()  # [K, N] per group
@@ -61,10 +71,10 @@ def test_rows_mnmajor_b(sizes, K, N):
         _close(C[off[g]:off[g + 1]], A[off[g]:off[g + 1]].float() @ B[g].float())
 
 
-def test_gelu_and_dgelu_epilogues():
+def test_gelu_and_dgelu_epilogues(cg):
     torch.manual_seed(2)
     sizes, K, N = [256, 128], 256, 512
-    off_t, off = _offsets(sizes)
+    off_t, off = _offsets([v * cg for v in sizes])
     rows, G = off[-1], len(sizes)
     A = torch.randn(rows, K, device="cuda").bfloat16()
     B = (torch.randn(G, N, K, device="cuda") / K ** 0.5).bfloat16()
@@ -87,7 +97,7 @@ def test_gelu_and_dgelu_epilogues():
         _close(dH[sl], (A[sl].float() @ B2[g].float()) * h.grad, rtol=2e-2)
 
 
-@pytest.mark.parametrize("sizes,M,N", [([128], 128, 256), ([64, 0, 192, 128], 256, 512),
+@pytest.mark.parametrize("sizes,M,N", [([128], 256, 256), ([64, 0, 192, 128], 256, 512),
                                        ([1024, 512], 1024, 256)])
 def test_wgrad_variable_k(sizes, M, N):
     torch.manual_seed(3)
@@ -107,14 +117,14 @@ def test_wgrad_variable_k(sizes, M, N):
             _close(C[g], ref)
 
 
-def test_persistent_grid_smaller_than_tiles():
+def test_persistent_grid_smaller_than_tiles(cg):
     torch.manual_seed(4)
-    off_t, off = _offsets([640, 384])
+    off_t, off = _offsets([640 * cg, 384 * cg])
     K, N = 192, 768
     A = torch.randn(off[-1], K, device="cuda").bfloat16()
     B = (torch.randn(2, N, K, device="cuda") / K ** 0.5).bfloat16()
     C = torch.empty((off[-1], N), device="cuda").bfloat16()
-    ops.grouped_gemm_rows(A, B, off_t, C, num_sms=3)  # 3 CTAs loop over 24 tiles
+    ops.grouped_gemm_rows(A, B, off_t, C, num_sms=4)  # 4 CTAs loop over 24 tiles
     torch.cuda.synchronize()
     for g in range(2):
         _close(C[off[g]:off[g + 1]], A[off[g]:off[g + 1]].float() @ B[g].float().t())
