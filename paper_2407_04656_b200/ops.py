@@ -213,3 +213,7 @@ def dispatch_bwd_p2p(peers_dxe, dest_rank, dest_row, probs, idx, dw, wg, renorm:
     _lib.call("lz_dispatch_bwd_p2p", ptr(peers_dxe), ptr(dest_rank), ptr(dest_row), Tn, d, k,
               ptr(probs), ptr(idx), ptr(dw), ptr(wg), E, int(renorm), ptr(dx), ptr(dlog), _s())
     return dx, dlog
+
+
+if "LZ_GEMM_CTA" in __import__("os").environ:  # A/B switch for the GEMM variant
+    set_gemm_cta_group(int(__import__("os").environ["LZ_GEMM_CTA"]))
