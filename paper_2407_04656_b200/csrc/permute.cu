@@ -421,7 +421,7 @@ static long pad_items(int E, const int32_t* recv_m, const int32_t* recv_off, int
 
 // Pad rows are enumerated per expert inside zero_pad_rows; we launch enough warp
 // items to cover the worst case of (align-1) pad rows per expert, align = 128.
-static constexpr int kPadAlign = 128;
+static constexpr int kPadAlign = 256;  // >= the largest GEMM row alignment (lz_gemm_row_align)
 
 static lz_status pack_impl(const void* x, int Tn, int d, int k, const int32_t* row,
                            const int32_t* prank, const unsigned long long* peers, void* out, int E,

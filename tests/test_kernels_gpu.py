@@ -61,19 +61,20 @@ def _rows(Tn, k, n_rows, gen):
     return torch.randperm(n_rows, generator=gen)[:Tn * k].int()
 
 
-def test_pack_exact_and_pad_zero():
+@pytest.mark.parametrize("m,off", [([2500, 0, 3500], [0, 2560, 2560, 6144]),      # 128-aligned
+                                   ([2049, 0, 3951], [0, 2304, 2304, 6400])])     # pads up to 255
+def test_pack_exact_and_pad_zero(m, off):
     gen = torch.Generator().manual_seed(5)
     Tn, d, k = 3000, 1024, 2
     x = torch.randn(Tn, d, generator=gen).bfloat16()
-    # expert-major padded layout: 3 experts with m = 2500, 0, 3500 (pads 60, 0, 84)
-    m = torch.tensor([2500, 0, 3500], dtype=torch.int32)
-    off = torch.tensor([0, 2560, 2560, 6144], dtype=torch.int32)
+    mt = torch.tensor(m, dtype=torch.int32)
+    ot = torch.tensor(off, dtype=torch.int32)
     perm = torch.randperm(6000, generator=gen)
-    real_rows = torch.cat([torch.arange(0, 2500), torch.arange(2560, 2560 + 3500)])
+    real_rows = torch.cat([torch.arange(off[e], off[e] + m[e]) for e in range(3)])
     row = real_rows[perm].int()
-    out = torch.full((6144, d), 7.0).bfloat16().cuda()
-    ops.pack(x.cuda(), row.cuda(), k, out, m.cuda(), off.cuda())
-    ref = torch.zeros(6144, d).bfloat16()
+    out = torch.full((off[-1], d), 7.0).bfloat16().cuda()
+    ops.pack(x.cuda(), row.cuda(), k, out, mt.cuda(), ot.cuda())
+    ref = torch.zeros(off[-1], d).bfloat16()
     ref[row.long()] = x.repeat_interleave(k, dim=0)
     assert torch.equal(out.cpu(), ref)
 
