@@ -34,6 +34,9 @@ class GraphedStep:
                     out.backward(self.dout[0])
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
+        # blocks freed with pending cross-stream uses (record_stream) are reclaimed by
+        # querying events -- illegal inside a capture; settle them now
+        torch.cuda.empty_cache()
         pool = None
         self.grads = []
         params = [p for p in layer.parameters() if p.requires_grad]
