@@ -273,6 +273,8 @@ def run_gpu(args, cfg):
         try:
             graph = GraphedStep(layer, Tn, nbuf=2, backward=cfg["bwd"])
         except Exception as exc:  # report, keep eager numbers
+            import traceback
+            traceback.print_exc()
             graph = None
             graph_err = repr(exc)[:200]
     if graph is not None:

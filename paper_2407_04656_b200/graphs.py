@@ -32,6 +32,7 @@ class GraphedStep:
                 out = layer(self.x[0])
                 if backward:
                     out.backward(self.dout[0])
+                del out  # no autograd node (AccumulateGrad) may outlive the iteration
         torch.cuda.current_stream(dev).wait_stream(side)
         torch.cuda.synchronize(dev)
         # blocks freed with pending cross-stream uses (record_stream) are reclaimed by
@@ -55,6 +56,7 @@ class GraphedStep:
             pool = g.pool()
             self.graphs.append(g)
             self.grads.append([p.grad for p in params])
+            del out
         self.params = params
 
     def replay(self, i: int = 0) -> torch.Tensor:
