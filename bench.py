@@ -247,7 +247,7 @@ def run_gpu(args, cfg):
             if i + 1 < nsteps:
                 pf.prefetch()
             out = step(xx, dd)
-            res_h.copy_(out.detach().float().sum().view(1), non_blocking=True)
+            res_h.copy_(out.detach().sum(dtype=torch.float32).view(1), non_blocking=True)
 
     e2e_run(2)
     torch.cuda.synchronize()

@@ -51,7 +51,7 @@ class GraphedStep:
                 if backward:
                     out.backward(self.dout[i])
                 # the step's scalar result (checksum of the layer output), read back by e2e
-                self.result[i] = out.detach().float().sum().view(1)
+                self.result[i] = out.detach().sum(dtype=torch.float32).view(1)
             self.launches_per_step = _lib.launch_count - l0
             pool = g.pool()
             self.graphs.append(g)
