@@ -268,7 +268,11 @@ def run_gpu(args, cfg):
     # step is captured once and replayed; value/ms_per_step/e2e come from it, the eager
     # numbers above are reported alongside.
     graph, graph_err = None, ""
-    if not args.no_graph:
+    if args.no_graph:
+        graph_err = "graphs disabled"
+    elif world > 1:
+        graph_err = "graph capture is used at N=1 only in this round"
+    else:
         from paper_2407_04656_b200.graphs import GraphedStep
         try:
             graph = GraphedStep(layer, Tn, nbuf=2, backward=cfg["bwd"])
@@ -381,7 +385,7 @@ def run_gpu(args, cfg):
                          "gemm_share_of_step": gemm_ms / ms if ms else None,
                          "gemms_per_step": gemms_per_step},
             "mode": "cuda-graph replay of the whole fwd+bwd step" if graph is not None
-                    else "eager (" + (graph_err if not args.no_graph else "graphs disabled") + ")",
+                    else "eager (" + graph_err + ")",
             "eager": eager,
             "e2e": {"value": world * Tn * args.steps / (ms_main_e2e * 1e-3), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(x.numel() * 2 + (dout.numel() * 2 if cfg["bwd"] else 0)),
