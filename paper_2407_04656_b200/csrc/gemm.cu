@@ -19,7 +19,8 @@ namespace lz {
 namespace gemm {
 
 constexpr int BM = 128, BN = 256, BK = 64;  // per-CTA rows, tile columns, k block
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;                       // 2 per TMEM lane quadrant (column halves)
+constexpr int kThreads = 64 + 32 * kEpiWarps;      // producer, MMA, epilogue warps
 constexpr int kAccCols = BN;              // fp32 accumulator columns per buffer
 constexpr int kTmemCols = 2 * kAccCols;   // 512
 constexpr int kMaxGroups = 128;
@@ -29,7 +30,7 @@ constexpr int kMaxGroups = 128;
 constexpr int kEpiCols = 32;
 constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
 constexpr int kEpiWarpBytes = 4 * kEpiBuf;          // out0 out1 aux0 aux1
-constexpr int kEpiBytes = 4 * kEpiWarpBytes;        // 32 KB
+constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;  // 64 KB
 constexpr int kBarBytes = 256;
 constexpr int kTabBytes = 2 * (kMaxGroups + 1) * 4;
 
@@ -43,7 +44,7 @@ struct Cfg {
   static constexpr int kATileBytes = BM * BK * 2;        // 16 KB
   static constexpr int kBTileBytes = kBRows * BK * 2;    // 32 KB / 16 KB
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kStages = CG == 1 ? 3 : 5;
   static constexpr int kTilesBytes = kStages * kStageBytes;
   static constexpr int kTileM = BM * CG;                 // rows per (pair) tile
   static constexpr int kSmemBytes = 1024 + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
@@ -337,8 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [4 warps][2 buffers]
-  uint32_t* s_tmem = (uint32_t*)(aux_bar + 8);
+  uint64_t* aux_bar = tempty_bar + 2;  // [epilogue warps][2 buffers]
+  uint32_t* s_tmem = (uint32_t*)(aux_bar + 2 * kEpiWarps);
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
@@ -368,9 +369,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], 4 * CG);  // one arrival per epilogue warp of each CTA
+      mbar_init(&tempty_bar[s], kEpiWarps * CG);  // one arrival per epilogue warp of each CTA
     }
-    for (int s = 0; s < 8; ++s) mbar_init(&aux_bar[s], 1);
+    for (int s = 0; s < 2 * kEpiWarps; ++s) mbar_init(&aux_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -471,21 +472,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===== epilogue warps 2..5: TMEM -> regs -> activation -> swizzled smem -> TMA store
-    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
-    uint8_t* wbuf = s_epi + quad * kEpiWarpBytes;
+    const int quad = warp & 3;          // TMEM lane quadrant this warp may access
+    const int ew = warp - 2;            // epilogue warp index
+    const int half = ew >> 2;           // column half of the tile this warp owns
+    uint8_t* wbuf = s_epi + ew * kEpiWarpBytes;
     const uint32_t out_s = smem_u32(wbuf);                 // out0, out1
     const uint32_t aux_s = smem_u32(wbuf + 2 * kEpiBuf);   // aux0, aux1
-    uint64_t* my_aux_bar = aux_bar + quad * 2;
+    uint64_t* my_aux_bar = aux_bar + ew * 2;
     uint32_t aux_phase[2] = {0, 0};
     const bool gelu = p.epilogue == LZ_EPI_GELU, dgelu = p.epilogue == LZ_EPI_DGELU;
-    constexpr int kChunks = BN / kEpiCols;
+    constexpr int kChunks = BN / kEpiCols / (kEpiWarps / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = unit; tile < total; tile += nunits) {
       const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
-      const int col0 = t.nb * BN;
+      const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
       if (dgelu && lane == 0) {
         // prefetch the first two pre-activation chunks of this tile
         fence_async_smem();
@@ -496,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols +
+                             half * (BN / (kEpiWarps / 4));
 #pragma unroll 1
       for (int c = 0; c < kChunks; ++c) {
         const int b = c & 1;
