@@ -1,0 +1,127 @@
+"""Multi-rank host logic on CPU (gloo, world_size 2 and 3): the load all-gather, the
+padding-free all-to-all-v in the reference's send order, the regroup into the padded
+expert-major receive layout, and the in-place replica-group gradient all-reduce.
+Device kernels are replaced by the oracle (the layout contract is what is tested)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import dispatch_ref as O
+from paper_2407_04656_b200 import comm
+from paper_2407_04656_b200.elastic import replan, transfer_schedule
+from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, n, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        E, k, d, P_tok = 6, 2, 8, 40
+        rng = np.random.default_rng(100 + rank)
+        routed = rng.choice(E, size=P_tok * k, p=np.array([.4, .2, .15, .1, .1, .05])).astype(np.int32)
+        hist = torch.from_numpy(np.bincount(routed, minlength=E).astype(np.int32))
+        # (1) load all-gather -> T [E, N]
+        T = comm.allgather_hist(hist)
+        allh = [torch.empty_like(hist) for _ in range(n)]
+        dist.all_gather(allh, hist)
+        assert torch.equal(T, torch.stack(allh, 1))
+        T_list = T.tolist()
+        R = replica_matrix(plan_for_loads(T.sum(1).tolist(), n, 4, 2))
+        sch = O.compute_dispatch_schedule(rank, T_list, R)
+        D_all = np.array(O.full_dispatch_matrices(T_list, R))
+        # (2) pack in the reference send order, all-to-all-v
+        x = torch.arange(P_tok, dtype=torch.float32).repeat_interleave(d).view(P_tok, d) + 1000 * rank
+        index = O.build_shuffle_index(sch["D"], routed)          # send slot -> assignment
+        send = x[torch.from_numpy(index // k)]
+        recv_counts = [int(D_all[j, :, rank].sum()) for j in range(n)]
+        stage = torch.empty(sum(recv_counts), d)
+        comm.all_to_all_rows(stage, send, recv_counts, sch["s"])
+        # (3) regroup into the expert-major, 4-row padded layout; check every row landed at
+        # the destination row the sender computed for it (source order kept)
+        m, pad_off, src_off = O.recv_layout(D_all, rank, align=4)
+        X = torch.full((int(pad_off[-1]), d), -1.0)
+        st = 0
+        for i in range(n):
+            for e in range(E):
+                c = int(D_all[i, e, rank])
+                X[src_off[e][i]:src_off[e][i] + c] = stage[st:st + c]
+                st += c
+        # every sender's rows: the tokens it routed to e that the plan gave to this rank
+        for i in range(n):
+            rng_i = np.random.default_rng(100 + i)
+            r_i = rng_i.choice(E, size=P_tok * k, p=np.array([.4, .2, .15, .1, .1, .05]))
+            idx_i = O.build_shuffle_index(O.compute_dispatch_schedule(i, T_list, R)["D"], r_i)
+            base = sum(int(D_all[i, :, j].sum()) for j in range(rank))
+            for e in range(E):
+                pre = sum(int(D_all[i, ee, rank]) for ee in range(e))
+                c = int(D_all[i, e, rank])
+                toks = idx_i[base + pre: base + pre + c] // k
+                want = torch.from_numpy(toks).float().repeat_interleave(d).view(c, d) + 1000 * i
+                assert torch.equal(X[src_off[e][i]:src_off[e][i] + c], want)
+        # (4) replica-group all-reduce in place (experts sharing an owner set share a group)
+        groups = comm.ReplicaGroups(R)
+        local = [e for e in range(E) if R[e][rank] > 0]
+        g1 = torch.stack([torch.full((3, 2), float(rank + 1) * (e + 1)) for e in local])
+        g2 = torch.stack([torch.full((2,), float(rank + 1)) for e in local])
+        groups.allreduce([g1, g2], local)
+        for p, e in enumerate(local):
+            owners = [j for j in range(n) if R[e][j] > 0]
+            want = sum(j + 1 for j in owners)
+            assert torch.allclose(g1[p], torch.full((3, 2), float(want * (e + 1))))
+            assert torch.allclose(g2[p], torch.full((2,), float(want)))
+        q.put((rank, "ok"))
+    except Exception as exc:  # surface to the parent
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_multirank_host_path_gloo(n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(n)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}:\n{msg}"
+
+
+def test_elastic_replan_and_transfers():
+    """8 -> 6 -> 4 host re-plan (reference recipe) and the state-transfer schedule."""
+    E, c = 16, 6
+    loads = [int(1000 * (1 + e) ** -1.2) + 10 for e in range(E)]
+    plan8 = plan_for_loads(loads, 8, c, 2)
+    holdings = {v: set(plan8.column(v)) for v in range(8)}
+    for live in ([0, 1, 2, 4, 5, 7], [0, 2, 4, 7]):
+        held = {v: holdings[v] for v in live}
+        plan, order, R = replan(loads, live, held, c, 2)
+        assert sorted(order) == sorted(live)
+        assert all(sum(row) > 0 for row in R)                       # every expert hosted
+        transfers, orphans = transfer_schedule(R, sorted(live), held)
+        for e, src, dst in transfers:
+            assert e in held[src] and e not in held[dst] and src != dst
+        newly = {(e, v) for r, v in enumerate(sorted(live)) for e in range(E)
+                 if R[e][r] > 0 and e not in held[v]}
+        assert newly == {(e, dst) for e, _, dst in transfers} | {(e, v) for e, v in orphans}
+        holdings = {v: {e for e in range(E) if R[e][r] > 0} for r, v in enumerate(sorted(live))}
