@@ -32,6 +32,8 @@ CONFIGS = {
                  name="CPU-ref MoE layer (E8 top-2 d512 d_ff2048, 1024 tok/rank, fwd)"),
     "cfg2": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=3, bwd=True,
                  name="GPT-MoE layer (E16 top-2 d1024 d_ff4096, 64K tok/GPU, fwd+bwd)"),
+    "cfg4": dict(E=64, k=1, d=2048, dff=None, tokens=131072, s=1.5, slot_factor=4, bwd=False,
+                 name="E64 top-1 d2048 dispatch/combine-only sweep (8K..1M tok/GPU, Zipf 1.5)"),
 }
 METRIC = "MoE-layer tokens/s (dispatch+FFN+combine, fwd+bwd)"
 
@@ -409,6 +411,91 @@ def run_gpu(args, cfg):
     return 0
 
 
+def run_dispatch_sweep(args, cfg):
+    """Config 4: gate -> plan -> pack -> combine only (identity expert), HBM roofline of
+    the pack and combine kernels over 8K..1M tokens/GPU.  N = 1 only."""
+    from paper_2407_04656_b200 import ops
+    from paper_2407_04656_b200.dispatch import plan_device
+    from paper_2407_04656_b200.layer import zipf_router_bias
+    from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix
+    rank, world, local = _env()
+    if rank != 0:
+        return 0
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    E, k, d = cfg["E"], cfg["k"], cfg["d"]
+    hbm, _, _, src = _peaks()
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    wg = (torch.randn(E, d, generator=g, device=dev) * 0.02).bfloat16()
+    bg = zipf_router_bias(E, cfg["s"]).to(dev)
+    sweep = []
+    for Tn in (8192, 16384, 32768, 65536, 131072, 262144, 524288, 1048576):
+        x = torch.randn(Tn, d, generator=g, device=dev).bfloat16()
+        idx, w, _, hist = ops.router_gate(x, wg, bg, k, probs=False)
+        loads = hist.tolist()
+        R = torch.tensor(replica_matrix(plan_for_loads(loads, 1, math.ceil(4 * E), 2)),
+                         dtype=torch.int32, device=dev)
+        align = ops.row_align()
+        P = Tn * k
+        X = torch.empty(P + E * align, d, dtype=torch.bfloat16, device=dev)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+
+        def once(rec):
+            if rec:
+                ev[0].record()
+            i2, w2, _, h2 = ops.router_gate(x, wg, bg, k, probs=False)
+            if rec:
+                ev[1].record()
+            pl = plan_device(h2.view(E, 1), R, 0, i2.view(-1), align)
+            if rec:
+                ev[2].record()
+            ops.pack(x, pl.dest_row, k, X, pl.recv_m, pl.recv_off)
+            if rec:
+                ev[3].record()
+            out = ops.combine(X, pl.dest_row, w2, k)
+            if rec:
+                ev[4].record()
+            return out
+
+        for _ in range(3):
+            once(False)
+        torch.cuda.synchronize()
+        reps = max(3, min(50, (1 << 22) // Tn))
+        acc = [0.0] * 4
+        for _ in range(reps):
+            once(True)
+            torch.cuda.synchronize()
+            for j in range(4):
+                acc[j] += ev[j].elapsed_time(ev[j + 1])
+        t_gate, t_plan, t_pack, t_comb = (a / reps for a in acc)
+        pack_b = Tn * d * 2 + P * d * 2 + P * 4
+        comb_b = P * d * 2 + P * 8 + Tn * d * 2
+        total = t_gate + t_plan + t_pack + t_comb
+        sweep.append({"tokens": Tn, "ms": round(total, 4), "tokens_per_s": Tn / (total * 1e-3),
+                      "gate_ms": round(t_gate, 4), "plan_ms": round(t_plan, 4),
+                      "pack_ms": round(t_pack, 4), "combine_ms": round(t_comb, 4),
+                      "pack_GBps": pack_b / (t_pack * 1e-3) / 1e9,
+                      "combine_GBps": comb_b / (t_comb * 1e-3) / 1e9,
+                      "pack_frac": pack_b / (t_pack * 1e-3) / 1e9 / hbm,
+                      "combine_frac": comb_b / (t_comb * 1e-3) / 1e9 / hbm})
+        del x, X
+    ref = next(r for r in sweep if r["tokens"] == cfg["tokens"])
+    line = {"metric": "dispatch+combine tokens/s (gate+plan+pack+combine, no FFN)",
+            "value": ref["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1, "steps": None,
+            "warmup": 3, "ms_per_step": ref["ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": cfg["name"], "experts": E, "top_k": k, "d_model": d,
+                       "tokens_per_gpu": cfg["tokens"]},
+            "roofline": {"kernel": "lz pack / combine", "bound": "hbm",
+                         "achieved": ref["pack_GBps"], "peak": hbm, "unit": "GB/s",
+                         "frac": ref["pack_frac"], "combine_frac": ref["combine_frac"],
+                         "peak_kind": f"{src} copy bandwidth", "traffic": None},
+            "sweep": sweep}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def plan_replicas(plan, E):
     counts = [0] * E
     for row in plan.slots:
@@ -431,6 +518,8 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.config == "cfg4":
+        return run_dispatch_sweep(args, cfg)
     return run_gpu(args, cfg)
 
 
