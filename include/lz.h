@@ -186,6 +186,10 @@ lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, in
 #define LZ_EPI_STORE 0     /* C = acc (bf16)                                   */
 #define LZ_EPI_GELU 1      /* C = gelu(acc), AUX = acc (pre-activation, bf16)  */
 #define LZ_EPI_DGELU 2     /* C = acc * gelu'(AUX)                             */
+#define LZ_EPI_SWIGLU 3    /* B rows = W1|W3 interleaved in 128-row blocks: AUX[rows, N] = acc
+                              (gate|up pre-activations), C[rows, N/2] = silu(gate) * up */
+#define LZ_EPI_DSWIGLU 4   /* acc = dA[rows, N]; AUX = interleaved pre-activations [rows, 2N];
+                              C[rows, 2N] = [dgate | dup] interleaved like AUX            */
 /* Operand majors */
 #define LZ_K_MAJOR 0
 #define LZ_MN_MAJOR 1

@@ -47,7 +47,7 @@ _RESTYPE = {"lz_status_string": ctypes.c_char_p, "lz_router_wgrad_ws_bytes": cty
 # header constants (include/lz.h)
 LZ_OK, LZ_ERR_ARG, LZ_ERR_UNROUTABLE, LZ_ERR_CUDA, LZ_ERR_WORKSPACE, LZ_ERR_UNSUPPORTED = range(6)
 LZ_ERRF_UNROUTABLE, LZ_ERRF_COUNTS, LZ_ERRF_EXPERT_ID = 1, 2, 4
-LZ_EPI_STORE, LZ_EPI_GELU, LZ_EPI_DGELU = 0, 1, 2
+LZ_EPI_STORE, LZ_EPI_GELU, LZ_EPI_DGELU, LZ_EPI_SWIGLU, LZ_EPI_DSWIGLU = 0, 1, 2, 3, 4
 LZ_K_MAJOR, LZ_MN_MAJOR = 0, 1
 LZ_MAX_RANKS, LZ_MAX_EXPERTS, LZ_MAX_EN, LZ_MAX_TOPK = 64, 1024, 4096, 8
 

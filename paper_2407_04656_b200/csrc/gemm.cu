@@ -323,6 +323,139 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
   return t;
 }
 
+// SwiGLU epilogues (Mixtral experts).  W1|W3 are interleaved in blocks of 128 output
+// rows, so one 256-wide N tile holds the gate (cols 0..127) and up (cols 128..255)
+// projections of the same 128 hidden units.
+//   SWIGLU : H[rows, N] = [G | U] pre-activations (aux, kept for backward),
+//            C[rows, N/2] = silu(G) * U at hidden column nb*128 + j
+//   DSWIGLU: GEMM output dA[rows, N] (N = d_ff, hidden units); reads G, U from the
+//            interleaved H[rows, 2N] and writes dH = [dG | dU] into C[rows, 2N]
+// Each epilogue warp owns 32 rows and one half of the tile's hidden units; single-
+// buffered staging (4 x 2 KB per warp), next chunk's G/U loads overlap the current chunk.
+__device__ __forceinline__ float sigmoid_f(float x) { return 0.5f * (1.f + tanh_fast(0.5f * x)); }
+
+__device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const TileInfo& t,
+                                             int row0, int half, int lane, uint32_t tbase,
+                                             uint64_t* tfull, uint32_t acc_phase,
+                                             uint64_t* tempty, uint8_t* wbuf, uint64_t* abar,
+                                             uint32_t& aphase, const CUtensorMap* map_c,
+                                             const CUtensorMap* map_x, int cg) {
+  const uint32_t s_out0 = smem_u32(wbuf), s_out1 = s_out0 + kEpiBuf;
+  const uint32_t s_aux0 = s_out0 + 2 * kEpiBuf, s_aux1 = s_out0 + 3 * kEpiBuf;
+  const int nchunks = fwd ? 2 : 4;  // 64 hidden units (fwd) / 128 hidden units (bwd) per warp
+  auto cols = [&](int c, int& gcol, int& ucol, int& hid) {
+    if (fwd) {
+      hid = t.nb * (BN / 2) + half * 64 + c * 32;              // Act column
+      gcol = t.nb * BN + half * 64 + c * 32;                   // gate column in H
+      ucol = gcol + BN / 2;
+    } else {
+      const int n0 = t.nb * BN + half * 128 + c * 32;          // hidden unit
+      hid = n0;
+      gcol = (n0 / 128) * 256 + (n0 % 128);
+      ucol = gcol + 128;
+    }
+  };
+  if (!fwd && lane == 0) {  // first chunk's pre-activations
+    int g, u, h;
+    cols(0, g, u, h);
+    fence_async_smem();
+    mbar_expect_tx(abar, 2 * kEpiBuf);
+    tma_load_2d(wbuf + 2 * kEpiBuf, map_x, abar, g, row0);
+    tma_load_2d(wbuf + 3 * kEpiBuf, map_x, abar, u, row0);
+  }
+  mbar_wait(tfull, acc_phase);
+  tc_fence_after();
+  for (int c = 0; c < nchunks; ++c) {
+    int gcol, ucol, hid;
+    cols(c, gcol, ucol, hid);
+    uint32_t va[32], vb[32];
+    if (fwd) {
+      tmem_ld32(tbase + half * 64 + c * 32, va);           // gate
+      tmem_ld32(tbase + BN / 2 + half * 64 + c * 32, vb);  // up
+    } else {
+      tmem_ld32(tbase + half * 128 + c * 32, va);          // dA
+    }
+    if (t.nk == 0) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) va[q] = vb[q] = 0u;
+    }
+    if (c == nchunks - 1) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (cg == 1) mbar_arrive(tempty);
+        else mbar_arrive_cluster(tempty, 0);
+      }
+    }
+    float g[32], u[32];
+    if (fwd) {
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        g[q] = __uint_as_float(va[q]);
+        u[q] = __uint_as_float(vb[q]);
+      }
+    } else {
+      mbar_wait(abar, aphase);
+      aphase ^= 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        bf16x8_to_f32(ld_shared_v4(s_aux0 + stg_off(lane, q)), g + 8 * q);
+        bf16x8_to_f32(ld_shared_v4(s_aux1 + stg_off(lane, q)), u + 8 * q);
+      }
+    }
+    if (lane == 0) bulk_wait_read<0>();  // staging buffers free again
+    __syncwarp();
+    if (!fwd && c + 1 < nchunks && lane == 0) {
+      int g2, u2, h2;
+      cols(c + 1, g2, u2, h2);
+      fence_async_smem();
+      mbar_expect_tx(abar, 2 * kEpiBuf);
+      tma_load_2d(wbuf + 2 * kEpiBuf, map_x, abar, g2, row0);
+      tma_load_2d(wbuf + 3 * kEpiBuf, map_x, abar, u2, row0);
+    }
+    if (fwd) {
+      float a[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) a[q] = g[q] * sigmoid_f(g[q]) * u[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        st_shared_v4(s_aux0 + stg_off(lane, q), f32_to_bf16x8(g + 8 * q));
+        st_shared_v4(s_aux1 + stg_off(lane, q), f32_to_bf16x8(u + 8 * q));
+        st_shared_v4(s_out0 + stg_off(lane, q), f32_to_bf16x8(a + 8 * q));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map_x, wbuf + 2 * kEpiBuf, gcol, row0);
+        tma_store_2d(map_x, wbuf + 3 * kEpiBuf, ucol, row0);
+        tma_store_2d(map_c, wbuf, hid, row0);
+        bulk_commit();
+      }
+    } else {
+      float dg[32], du[32];
+#pragma unroll
+      for (int q = 0; q < 32; ++q) {
+        const float da = __uint_as_float(va[q]);
+        const float sg = sigmoid_f(g[q]);
+        du[q] = da * g[q] * sg;
+        dg[q] = da * u[q] * sg * (1.f + g[q] * (1.f - sg));
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        st_shared_v4(s_out0 + stg_off(lane, q), f32_to_bf16x8(dg + 8 * q));
+        st_shared_v4(s_out1 + stg_off(lane, q), f32_to_bf16x8(du + 8 * q));
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_2d(map_c, wbuf, gcol, row0);
+        tma_store_2d(map_c, wbuf + kEpiBuf, ucol, row0);
+        bulk_commit();
+      }
+    }
+  }
+}
+
 template <int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -481,6 +614,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* my_aux_bar = aux_bar + ew * 2;
     uint32_t aux_phase[2] = {0, 0};
     const bool gelu = p.epilogue == LZ_EPI_GELU, dgelu = p.epilogue == LZ_EPI_DGELU;
+    const bool swiglu = p.epilogue == LZ_EPI_SWIGLU, dswiglu = p.epilogue == LZ_EPI_DSWIGLU;
     constexpr int kChunks = BN / kEpiCols / (kEpiWarps / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -496,6 +630,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&my_aux_bar[c], kEpiBuf);
           tma_load_2d(wbuf + (2 + c) * kEpiBuf, &map_x, &my_aux_bar[c], col0 + c * kEpiCols, row0);
         }
+      }
+      if (swiglu || dswiglu) {
+        swiglu_epilogue(p, swiglu, t, row0, half, lane, tmem_base + ((uint32_t)(quad * 32) << 16) +
+                        acc * kAccCols, &tfull_bar[acc], acc_phase, &tempty_bar[acc], wbuf,
+                        my_aux_bar, aux_phase[0], &map_c, &map_x, CG);
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
@@ -677,7 +821,7 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
                                      int c_group_rows, int c_row_offset, void* stream) {
   if (G < 1 || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
   if (G > kMaxGroups) return LZ_ERR_UNSUPPORTED;
-  if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DGELU) return LZ_ERR_ARG;
+  if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DSWIGLU) return LZ_ERR_ARG;
   if ((epilogue != LZ_EPI_STORE) && (mode != 0 || !aux)) return LZ_ERR_ARG;
   if (N <= 0 || N % BN) return LZ_ERR_UNSUPPORTED;
   const int tile_m = BM * g_cta_group;
@@ -706,8 +850,12 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
     } else {
       if (!make_map(&mb, B, N, (uint64_t)G * K, 64, BK)) return LZ_ERR_CUDA;
     }
-    if (!make_map(&mc, C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
-    if (!make_map(&mx, aux ? aux : C, N, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
+    // output / aux widths: SWIGLU writes C[rows, N/2] and H[rows, N]; DSWIGLU reads and
+    // writes the interleaved [rows, 2N]
+    const uint64_t c_w = epilogue == LZ_EPI_SWIGLU ? N / 2 : (epilogue == LZ_EPI_DSWIGLU ? 2 * N : N);
+    const uint64_t x_w = epilogue == LZ_EPI_DSWIGLU ? 2 * N : N;
+    if (!make_map(&mc, C, c_w, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
+    if (!make_map(&mx, aux ? aux : C, x_w, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     // upper bound of tiles; the kernel reads the exact count from the device offsets
     long tiles = (long)(rows_total / tile_m) * (N / BN);
     return b_major == LZ_K_MAJOR ? launch_cg<0, 0>(ma, mb, mc, mx, p, tiles, sms, s)

@@ -144,3 +144,45 @@ def test_wgrad_interleaved_output():
         sl = slice(off[g], off[g + 1])
         _close(buf[g, M:2 * M], A[sl].float().t() @ B[sl].float())
         assert (buf[g, :M] == 0).all() and (buf[g, 2 * M:] == 0).all()
+
+
+def _interleave(w1, w3):
+    """[G, F, K] x2 -> [G, 2F, K] with 128-row blocks alternating gate / up."""
+    G, F, K = w1.shape
+    return torch.stack([w1.view(G, F // 128, 128, K), w3.view(G, F // 128, 128, K)],
+                       dim=2).reshape(G, 2 * F, K)
+
+
+def test_swiglu_epilogues(cg):
+    torch.manual_seed(6)
+    sizes, K, F = [256, 512], 256, 512
+    off_t, off = _offsets([v * cg for v in sizes])
+    rows, G = off[-1], len(sizes)
+    X = torch.randn(rows, K, device="cuda").bfloat16()
+    w1 = (torch.randn(G, F, K, device="cuda") / K ** 0.5).bfloat16()
+    w3 = (torch.randn(G, F, K, device="cuda") / K ** 0.5).bfloat16()
+    W13 = _interleave(w1, w3).contiguous()
+    H = torch.empty(rows, 2 * F, device="cuda").bfloat16()
+    Act = torch.empty(rows, F, device="cuda").bfloat16()
+    ops.grouped_gemm_rows(X, W13, off_t, Act, epilogue=_lib.LZ_EPI_SWIGLU, aux=H)
+    # backward epilogue: dA = X . B2 (B2 [G, K, F] MN-major), dH = d[silu(g) u]
+    B2 = (torch.randn(G, K, F, device="cuda") / K ** 0.5).bfloat16()
+    dH = torch.empty(rows, 2 * F, device="cuda").bfloat16()
+    ops.grouped_gemm_rows(X, B2, off_t, dH, b_major=_lib.LZ_MN_MAJOR,
+                          epilogue=_lib.LZ_EPI_DSWIGLU, aux=H)
+    torch.cuda.synchronize()
+    for g in range(G):
+        sl = slice(off[g], off[g + 1])
+        xg = X[sl].float()
+        gate, up = xg @ w1[g].float().t(), xg @ w3[g].float().t()
+        Hi = H[sl].view(-1, F // 128, 2, 128)
+        _close(Hi[:, :, 0].reshape(-1, F), gate)
+        _close(Hi[:, :, 1].reshape(-1, F), up)
+        gb, ub = Hi[:, :, 0].reshape(-1, F).float(), Hi[:, :, 1].reshape(-1, F).float()
+        _close(Act[sl], torch.nn.functional.silu(gb) * ub, rtol=2e-2)
+        gq, uq = gb.clone().requires_grad_(True), ub.clone().requires_grad_(True)
+        dA = xg @ B2[g].float()
+        (torch.nn.functional.silu(gq) * uq).backward(dA)
+        dHi = dH[sl].view(-1, F // 128, 2, 128)
+        _close(dHi[:, :, 0].reshape(-1, F), gq.grad, rtol=2e-2)
+        _close(dHi[:, :, 1].reshape(-1, F), uq.grad, rtol=2e-2)
