@@ -30,12 +30,15 @@ def gelu(x: torch.Tensor) -> torch.Tensor:
     return torch.nn.functional.gelu(x, approximate="tanh")
 
 
-def ffn_ref(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor) -> torch.Tensor:
-    """One expert: gelu(x W1^T) W2^T with W1 [d_ff, d], W2 [d, d_ff] (fp32)."""
-    return gelu(x @ w1.t()) @ w2.t()
+def ffn_ref(x: torch.Tensor, w1: torch.Tensor, w2: torch.Tensor, w3=None) -> torch.Tensor:
+    """One expert: gelu(x W1^T) W2^T (GPT) or (silu(x W1^T) * x W3^T) W2^T (Mixtral);
+    W1, W3 [d_ff, d], W2 [d, d_ff] (fp32)."""
+    if w3 is None:
+        return gelu(x @ w1.t()) @ w2.t()
+    return (torch.nn.functional.silu(x @ w1.t()) * (x @ w3.t())) @ w2.t()
 
 
-def moe_forward_ref(x, wg, bg, w1, w2, k: int, renorm: bool = False, idx=None):
+def moe_forward_ref(x, wg, bg, w1, w2, k: int, renorm: bool = False, idx=None, w3=None):
     """Full layer in fp32 on the CPU.  x [T, d]; wg [E, d]; bg [E]; w1 [E, d_ff, d];
     w2 [E, d, d_ff].  Returns (out, idx, w, probs).  Differentiable w.r.t. all inputs
     (the top-k selection is treated as constant, as in the GPU backward).  If ``idx``
@@ -53,6 +56,6 @@ def moe_forward_ref(x, wg, bg, w1, w2, k: int, renorm: bool = False, idx=None):
         tok, slot = (idx == e).nonzero(as_tuple=True)
         if tok.numel() == 0:
             continue
-        y = ffn_ref(x[tok], w1[e], w2[e])
+        y = ffn_ref(x[tok], w1[e], w2[e], None if w3 is None else w3[e])
         out = out.index_add(0, tok, y * w[tok, slot].unsqueeze(1))
     return out, idx.to(torch.int32), w, probs

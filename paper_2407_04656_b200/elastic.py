@@ -93,7 +93,8 @@ def shrink_and_replan(layer, group, exclude: Sequence[int], loads: Sequence[int]
             ops.append(dist.P2POp(dist.isend, w1.contiguous(), rank_of[dst], new_group))
             ops.append(dist.P2POp(dist.isend, w2.contiguous(), rank_of[dst], new_group))
         elif dst == me:
-            b1 = torch.empty((layer.d_ff, layer.d), dtype=torch.bfloat16, device=layer.device)
+            f1 = 2 * layer.d_ff if layer.activation == "swiglu" else layer.d_ff
+            b1 = torch.empty((f1, layer.d), dtype=torch.bfloat16, device=layer.device)
             b2 = torch.empty((layer.d, layer.d_ff), dtype=torch.bfloat16, device=layer.device)
             ops.append(dist.P2POp(dist.irecv, b1, rank_of[src], new_group))
             ops.append(dist.P2POp(dist.irecv, b2, rank_of[src], new_group))

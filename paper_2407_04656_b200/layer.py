@@ -41,11 +41,41 @@ def _expert_weights(seed: int, e: int, shape, std: float, device) -> torch.Tenso
     return (torch.randn(shape, generator=g, device=device) * std).to(torch.bfloat16)
 
 
+def interleave_swiglu(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """W1 (gate), W3 (up) [..., F, K] -> [..., 2F, K], alternating 128-row blocks, so one
+    256-wide GEMM N tile carries gate and up of the same 128 hidden units."""
+    F, K = w1.shape[-2:]
+    lead = w1.shape[:-2]
+    return torch.stack([w1.reshape(*lead, F // 128, 128, K), w3.reshape(*lead, F // 128, 128, K)],
+                       dim=-3).reshape(*lead, 2 * F, K)
+
+
+def deinterleave_swiglu(w13: torch.Tensor):
+    F2, K = w13.shape[-2:]
+    lead = w13.shape[:-2]
+    v = w13.reshape(*lead, F2 // 256, 2, 128, K)
+    return v[..., 0, :, :].reshape(*lead, F2 // 2, K), v[..., 1, :, :].reshape(*lead, F2 // 2, K)
+
+
+def init_expert(seed: int, e: int, d: int, d_ff: int, std: float, device, activation: str):
+    """Deterministic expert e weights (identical on every owner rank)."""
+    if activation == "gelu":
+        return (_expert_weights(seed, 2 * e, (d_ff, d), std, device),
+                _expert_weights(seed, 2 * e + 1, (d, d_ff), std, device))
+    w1 = _expert_weights(seed, 3 * e, (d_ff, d), std, device)
+    w3 = _expert_weights(seed, 3 * e + 1, (d_ff, d), std, device)
+    return interleave_swiglu(w1, w3), _expert_weights(seed, 3 * e + 2, (d, d_ff), std, device)
+
+
 class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int = 2, *,
                  replicas=None, group=None, renorm: bool = False, seed: int = 0,
-                 init_std: float = 0.02, router_bias=None, device=None, exchange: str | None = None):
+                 init_std: float = 0.02, router_bias=None, device=None, exchange: str | None = None,
+                 activation: str = "gelu"):
         super().__init__()
+        if activation not in ("gelu", "swiglu"):
+            raise ValueError("activation must be 'gelu' (GPT MLP) or 'swiglu' (Mixtral)")
+        self.activation = activation
         if d_model % 256 or d_ff % 256:
             raise ValueError("d_model and d_ff must be multiples of 256 (GEMM tile)")
         if not 1 <= top_k <= min(n_experts, _lib.LZ_MAX_TOPK) or n_experts > 64:
@@ -108,12 +138,12 @@ class MoELayer(torch.nn.Module):
             elif e in old:
                 a, b = old[e]
             else:
-                a = _expert_weights(self.seed, 2 * e, (self.d_ff, self.d), self.init_std, self.device)
-                b = _expert_weights(self.seed, 2 * e + 1, (self.d, self.d_ff), self.init_std,
-                                    self.device)
+                a, b = init_expert(self.seed, e, self.d, self.d_ff, self.init_std, self.device,
+                                   self.activation)
             w1s.append(a)
             w2s.append(b)
-        # w1[g] = W1_e [d_ff, d], w2[g] = W2_e [d, d_ff] (row-major, K contiguous for fwd)
+        # gelu:   w1[g] = W1_e [d_ff, d];  swiglu: w1[g] = W1_e|W3_e interleaved in 128-row
+        # blocks [2 d_ff, d];  w2[g] = W2_e [d, d_ff] (row-major, K contiguous for fwd)
         self.w1 = torch.nn.Parameter(torch.stack(w1s).contiguous())
         self.w2 = torch.nn.Parameter(torch.stack(w2s).contiguous())
         self.replica_groups = comm.ReplicaGroups(R, self.group) if self.world > 1 else None
@@ -237,10 +267,12 @@ class _MoEFunction(torch.autograd.Function):
             del send, stage
         _mark(layer, "dispatch")
         d_ff = layer.d_ff
-        H = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
+        swi = layer.activation == "swiglu"
+        H = torch.empty((cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16, device=x.device)
         A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
         if G > 0:
-            ops.grouped_gemm_rows(X, w1, off, A, epilogue=_lib.LZ_EPI_GELU, aux=H)
+            ops.grouped_gemm_rows(X, w1, off, A, aux=H,
+                                  epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
             ops.grouped_gemm_rows(A, w2, off, Y)
         _mark(layer, "ffn_fwd")
         if mode == "local":
@@ -304,13 +336,14 @@ class _MoEFunction(torch.autograd.Function):
                               max_seg)
             del dret, stage
         _mark(layer, "combine_bwd")
-        dH = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=dev)
+        swi = layer.activation == "swiglu"
+        dH = torch.empty_like(H)
         dW1 = torch.empty_like(w1)
         dW2 = torch.empty_like(w2)
         if G > 0:
-            # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * gelu'(H)
-            ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR,
-                                  epilogue=_lib.LZ_EPI_DGELU, aux=H)
+            # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H)
+            ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
+                                  epilogue=_lib.LZ_EPI_DSWIGLU if swi else _lib.LZ_EPI_DGELU)
             # dX = dH . W1 (W1_e [d_ff, d] read MN-major)
             ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR)
             # variable-K weight gradients: dW1_e = dH_e^T X_e, dW2_e = dY_e^T A_e

@@ -24,13 +24,14 @@ def _rel(got, ref, l2=3e-2, linf=6e-2, name=""):
     assert e2 <= l2 and einf <= linf, f"{name}: rel l2 {e2:.3e} rel linf {einf:.3e}"
 
 
-@pytest.mark.parametrize("Tn,d,dff,E,k,s,renorm", [(1024, 512, 2048, 8, 2, 1.2, False),
-                                                  (2048, 1024, 4096, 16, 2, 2.5, False),
-                                                  (777, 512, 1024, 8, 1, 0.0, True)])
-def test_layer_matches_oracle(Tn, d, dff, E, k, s, renorm):
+@pytest.mark.parametrize("Tn,d,dff,E,k,s,renorm,act", [(1024, 512, 2048, 8, 2, 1.2, False, "gelu"),
+                                                      (2048, 1024, 4096, 16, 2, 2.5, False, "gelu"),
+                                                      (777, 512, 1024, 8, 1, 0.0, True, "gelu"),
+                                                      (1024, 512, 1024, 8, 2, 1.2, True, "swiglu")])
+def test_layer_matches_oracle(Tn, d, dff, E, k, s, renorm, act):
     torch.manual_seed(0)
     layer = MoELayer(d, dff, E, k, renorm=renorm, seed=3, init_std=0.05,
-                     router_bias=zipf_router_bias(E, s, seed=1))
+                     router_bias=zipf_router_bias(E, s, seed=1), activation=act)
     # load-based replicas on one rank (c = 3E slots): R[e][0] = r_e
     layer.set_plan(replica_matrix(plan_for_loads([100 * (e + 1) for e in range(E)], 1, 3 * E)))
     x = torch.randn(Tn, d, device="cuda").bfloat16().requires_grad_(True)
@@ -57,14 +58,22 @@ def test_layer_matches_oracle(Tn, d, dff, E, k, s, renorm):
     xr = xf.clone().requires_grad_(True)
     wg = layer.wg.detach().float().cpu().requires_grad_(True)
     bg = layer.bg.detach().float().cpu().requires_grad_(True)
+    from paper_2407_04656_b200.layer import deinterleave_swiglu, interleave_swiglu
     w1 = torch.zeros(E, dff, d)
+    w3 = torch.zeros(E, dff, d) if act == "swiglu" else None
     w2 = torch.zeros(E, d, dff)
     for p, e in enumerate(layer.local_ids):
-        w1[e] = layer.w1.detach()[p].float().cpu()
+        if act == "swiglu":
+            a, b = deinterleave_swiglu(layer.w1.detach()[p].float().cpu())
+            w1[e], w3[e] = a, b
+        else:
+            w1[e] = layer.w1.detach()[p].float().cpu()
         w2[e] = layer.w2.detach()[p].float().cpu()
     w1.requires_grad_(True)
     w2.requires_grad_(True)
-    ref, _, _, _ = moe_ref.moe_forward_ref(xr, wg, bg, w1, w2, k, renorm, idx=gidx)
+    if w3 is not None:
+        w3.requires_grad_(True)
+    ref, _, _, _ = moe_ref.moe_forward_ref(xr, wg, bg, w1, w2, k, renorm, idx=gidx, w3=w3)
     ref.backward(dout.float().cpu())
     _rel(out, ref, name="out")
     _rel(x.grad, xr.grad, name="dx")
@@ -76,7 +85,8 @@ def test_layer_matches_oracle(Tn, d, dff, E, k, s, renorm):
         _rel(layer.wg.grad, wg.grad, l2=5e-2, linf=1e-1, name="dwg")
         _rel(layer.bg.grad, bg.grad, l2=5e-2, linf=1e-1, name="dbg")
     for p, e in enumerate(layer.local_ids):
-        _rel(layer.w1.grad[p], w1.grad[e], name=f"dW1[{e}]")
+        want1 = w1.grad[e] if w3 is None else interleave_swiglu(w1.grad[e], w3.grad[e])
+        _rel(layer.w1.grad[p], want1, name=f"dW1[{e}]")
         _rel(layer.w2.grad[p], w2.grad[e], name=f"dW2[{e}]")
 
 
