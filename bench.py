@@ -32,6 +32,10 @@ CONFIGS = {
                  name="CPU-ref MoE layer (E8 top-2 d512 d_ff2048, 1024 tok/rank, fwd)"),
     "cfg2": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=3, bwd=True,
                  name="GPT-MoE layer (E16 top-2 d1024 d_ff4096, 64K tok/GPU, fwd+bwd)"),
+    "cfg3": dict(E=8, k=2, d=4096, dff=14336, tokens=16384, s=1.2, slot_factor=3, bwd=True,
+                 act="swiglu", cpu_tokens=256, cpu_reps=1,
+                 name="Mixtral-8x7B-shape MoE layer (E8 top-2 d4096 d_ff14336 SwiGLU, 16K tok/GPU, "
+                      "fwd+bwd + replica-group grad all-reduce)"),
     "cfg4": dict(E=64, k=1, d=2048, dff=None, tokens=131072, s=1.5, slot_factor=4, bwd=False,
                  name="E64 top-1 d2048 dispatch/combine-only sweep (8K..1M tok/GPU, Zipf 1.5)"),
 }
@@ -120,7 +124,8 @@ def cpu_reference(cfg, n_ranks, tokens_per_rank, reps, threads, seed=0):
     c = math.ceil(cfg["slot_factor"] * E / n_ranks)
     R = replica_matrix(plan_for_loads(loads, n_ranks, c, 2))
     return cpu_path.run(tokens_per_rank, n_ranks, E, cfg["d"], cfg["dff"], cfg["k"], R, reps=reps,
-                        seed=seed, bias=bias, backward=cfg["bwd"], threads=threads)
+                        seed=seed, bias=bias, backward=cfg["bwd"], threads=threads,
+                        activation=cfg.get("act", "gelu"))
 
 
 def run_reference(args, cfg):
@@ -129,7 +134,7 @@ def run_reference(args, cfg):
         return 0
     threads = len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
-    sample = 2048 if cfg["bwd"] else cfg["tokens"]
+    sample = cfg.get("cpu_tokens", 2048) if cfg["bwd"] else cfg["tokens"]
     n_virtual = 1 if args.config != "cfg1" else 4
     per_rank = sample // n_virtual if args.config != "cfg1" else cfg["tokens"]
     for _ in range(args.warmup):
@@ -172,7 +177,8 @@ def run_gpu(args, cfg):
     E, k, d, dff, Tn = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["tokens"]
     c = math.ceil(cfg["slot_factor"] * E / world)
     bias = zipf_router_bias(E, cfg["s"], seed=0)
-    layer = MoELayer(d, dff, E, k, seed=0, router_bias=bias, device=dev,
+    act = cfg.get("act", "gelu")
+    layer = MoELayer(d, dff, E, k, seed=0, router_bias=bias, device=dev, activation=act,
                      group=None if world == 1 else dist.group.WORLD)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -347,8 +353,10 @@ def run_gpu(args, cfg):
         hbm, tf_burst, tf_sus, src = _peaks()
         P = Tn * k
         gemms_per_step = 6 if cfg["bwd"] else 2
-        flops_per_launch = 2.0 * P * d * dff
-        achieved = flops_per_launch * n_gemm / (gemm_ms * 1e-3) / 1e12
+        n_mat = 3 if act == "swiglu" else 2
+        flops_per_step = 2.0 * P * d * dff * n_mat * (3 if cfg["bwd"] else 1)
+        flops_per_launch = flops_per_step / gemms_per_step
+        achieved = flops_per_step * args.steps / (gemm_ms * 1e-3) / 1e12
         traffic = None
         prof = os.path.join(ROOT, "profiles", "gemm_traffic.json")
         if os.path.exists(prof):
@@ -399,12 +407,14 @@ def run_gpu(args, cfg):
         }
         if world == 1 and not args.no_cpu_baseline:
             threads = len(os.sched_getaffinity(0))
-            tps, dt, tok = cpu_reference(cfg, 1, 4096 if cfg["bwd"] else Tn,
-                                         args.cpu_reps, threads)
+            ctok = cfg.get("cpu_tokens", 4096 if cfg["bwd"] else Tn)
+            reps = cfg.get("cpu_reps", args.cpu_reps)
+            tps, dt, tok = cpu_reference(cfg, 1, ctok, reps, threads)
             line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": threads,
                                     "kind": "port",
-                                    "sample": f"{tok} tokens ({args.cpu_reps} x 4096) of the "
-                                              f"same layer fwd+bwd on 1 rank, {dt:.1f} s"}
+                                    "sample": f"{tok} tokens ({reps} x {ctok}) of the "
+                                              f"same layer {'fwd+bwd' if cfg['bwd'] else 'fwd'} "
+                                              f"on 1 rank, {dt:.1f} s"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
