@@ -215,6 +215,9 @@ lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void*
 /* GEMM variant: 2 = CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles; default),
  * 1 = single-CTA kernel (128-row tiles).  Returns the active value. */
 int lz_gemm_set_cta_group(int cta_group);
+/* Epilogue store path: 1 = registers -> global (no smem staging), 0 = swizzled smem
+ * staging + TMA bulk-tensor stores (default).  Returns the active value. */
+int lz_gemm_set_direct_epilogue(int on);
 /* Row alignment mode-0 group segments must have for the active variant (128 or 256). */
 int lz_gemm_row_align(void);
 

@@ -40,6 +40,7 @@ _SIGS = {
     "lz_router_wgrad": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _sz, _vp],
     "lz_gemm_set_cta_group": [_i],
     "lz_gemm_row_align": [],
+    "lz_gemm_set_direct_epilogue": [_i],
     "lz_grouped_gemm": [_i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _vp],
 }
 _RESTYPE = {"lz_status_string": ctypes.c_char_p, "lz_router_wgrad_ws_bytes": ctypes.c_size_t}

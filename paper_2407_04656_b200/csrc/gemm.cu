@@ -273,6 +273,10 @@ struct Params {
   int M, N, K;      // mode 0: N, K used; mode 1: M, N
   const int32_t* off;
   int epilogue;
+  int direct;              // 1: epilogue stores straight from registers (no smem staging)
+  __nv_bfloat16* C;        // direct epilogue: output base and row stride (elements)
+  __nv_bfloat16* aux;
+  long ldc, ldx;
 };
 
 // A tile load (128 x 64) for the current stage
@@ -623,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
-      if (dgelu && lane == 0) {
+      if (dgelu && !p.direct && lane == 0) {
         // prefetch the first two pre-activation chunks of this tile
         fence_async_smem();
         for (int c = 0; c < 2; ++c) {
@@ -667,6 +671,34 @@ __global__ void __launch_bounds__(kThreads, 1)
         float f[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+        if (p.direct) {
+          // row-per-thread 16-byte stores: 4 x 16 B of this thread's row per 32 columns
+          const long grow = row0 + lane;
+          __nv_bfloat16* crow = p.C + grow * p.ldc + col0 + c * kEpiCols;
+          if (dgelu) {
+            const __nv_bfloat16* hrow = p.aux + grow * p.ldx + col0 + c * kEpiCols;
+            uint4 hv[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) hv[q] = ld_nc_v4(hrow + 8 * q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float h[8];
+              bf16x8_to_f32(hv[q], h);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
+            }
+          }
+          if (gelu) {
+            __nv_bfloat16* xrow = p.aux + grow * p.ldx + col0 + c * kEpiCols;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st_v4(xrow + 8 * q, f32_to_bf16x8(f + 8 * q));
+#pragma unroll
+            for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) st_v4(crow + 8 * q, f32_to_bf16x8(f + 8 * q));
+          continue;
+        }
         if (dgelu) {
           mbar_wait(&my_aux_bar[b], aux_phase[b]);
           aux_phase[b] ^= 1;
@@ -767,6 +799,12 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 }
 
 static int g_cta_group = 2;  // default: CTA-pair kernel
+static int g_direct_epi = 0;  // 1: register -> global epilogue, 0: smem staging + TMA store
+
+extern "C" int lz_gemm_set_direct_epilogue(int on) {
+  if (on == 0 || on == 1) g_direct_epi = on;
+  return g_direct_epi;
+}
 
 extern "C" int lz_gemm_set_cta_group(int cg) {
   if (cg == 1 || cg == 2) g_cta_group = cg;
@@ -836,6 +874,11 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.epilogue = epilogue;
   p.c_grp_rows = c_group_rows > 0 ? c_group_rows : M;
   p.c_row_off = c_row_offset;
+  p.direct = g_direct_epi && epilogue <= LZ_EPI_DGELU;
+  p.C = (__nv_bfloat16*)C;
+  p.aux = (__nv_bfloat16*)aux;
+  p.ldc = N;
+  p.ldx = N;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (sms < 2) sms = 2;

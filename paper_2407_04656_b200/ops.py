@@ -215,5 +215,11 @@ def dispatch_bwd_p2p(peers_dxe, dest_rank, dest_row, probs, idx, dw, wg, renorm:
     return dx, dlog
 
 
+def set_gemm_direct_epilogue(on: int) -> int:
+    return int(_lib.raw("lz_gemm_set_direct_epilogue", int(on)))
+
+
 if "LZ_GEMM_CTA" in __import__("os").environ:  # A/B switch for the GEMM variant
     set_gemm_cta_group(int(__import__("os").environ["LZ_GEMM_CTA"]))
+if "LZ_GEMM_DIRECT" in __import__("os").environ:  # A/B switch for the epilogue store path
+    set_gemm_direct_epilogue(int(__import__("os").environ["LZ_GEMM_DIRECT"]))
