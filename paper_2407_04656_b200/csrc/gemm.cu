@@ -671,7 +671,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         float f[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-        if (p.direct) {
+        if (p.direct == 2 && dgelu) {
+          // pre-activation read straight from global (row per thread), staged stores below
+          const __nv_bfloat16* hrow = p.aux + (long)(row0 + lane) * p.ldx + col0 + c * kEpiCols;
+          uint4 hv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hv[q] = ld_nc_v4(hrow + 8 * q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            float h[8];
+            bf16x8_to_f32(hv[q], h);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
+          }
+        }
+        if (p.direct == 1) {
           // row-per-thread 16-byte stores: 4 x 16 B of this thread's row per 32 columns
           const long grow = row0 + lane;
           __nv_bfloat16* crow = p.C + grow * p.ldc + col0 + c * kEpiCols;
@@ -699,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int q = 0; q < 4; ++q) st_v4(crow + 8 * q, f32_to_bf16x8(f + 8 * q));
           continue;
         }
-        if (dgelu) {
+        if (dgelu && p.direct == 0) {
           mbar_wait(&my_aux_bar[b], aux_phase[b]);
           aux_phase[b] ^= 1;
 #pragma unroll
@@ -713,7 +727,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the store that used buffer b (chunk c-2) must have finished reading smem
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        if (dgelu && c + 2 < kChunks && lane == 0) {
+        if (dgelu && p.direct == 0 && c + 2 < kChunks && lane == 0) {
           fence_async_smem();
           mbar_expect_tx(&my_aux_bar[b], kEpiBuf);
           tma_load_2d(wbuf + (2 + b) * kEpiBuf, &map_x, &my_aux_bar[b],
@@ -802,7 +816,7 @@ static int g_cta_group = 2;  // default: CTA-pair kernel
 static int g_direct_epi = 0;  // 1: register -> global epilogue, 0: smem staging + TMA store
 
 extern "C" int lz_gemm_set_direct_epilogue(int on) {
-  if (on == 0 || on == 1) g_direct_epi = on;
+  if (on >= 0 && on <= 2) g_direct_epi = on;
   return g_direct_epi;
 }
 
@@ -874,7 +888,7 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.epilogue = epilogue;
   p.c_grp_rows = c_group_rows > 0 ? c_group_rows : M;
   p.c_row_off = c_row_offset;
-  p.direct = g_direct_epi && epilogue <= LZ_EPI_DGELU;
+  p.direct = epilogue <= LZ_EPI_DGELU ? g_direct_epi : 0;
   p.C = (__nv_bfloat16*)C;
   p.aux = (__nv_bfloat16*)aux;
   p.ldc = N;

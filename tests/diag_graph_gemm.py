@@ -40,7 +40,7 @@ for epi, direct in ((0, 0), (0, 1), (1, 0), (1, 1)):
 
 # dgrad-like: MN-major B with DGELU epilogue
 Bm = torch.randn(G, K, N, device="cuda").bfloat16() * 0.03
-for direct in (0, 1):
+for direct in (0, 1, 2):
     ops.set_gemm_direct_epilogue(direct)
     f = lambda: ops.grouped_gemm_rows(A, Bm, off, C, b_major=1, epilogue=2, aux=H)
     f(); torch.cuda.synchronize()
