@@ -20,7 +20,7 @@ from .moe_ref import gate_ref, gelu
 
 def make_weights(E, d, dff, seed=0, std=0.02, bias=None, activation="gelu"):
     g = torch.Generator().manual_seed(seed)
-    wg = (torch.randn(E, d, generator=g) * std).requires_grad_(True)
+    wg = (torch.randn(E, d, generator=g) * (1.28 / d ** 0.5)).requires_grad_(True)
     bg = (torch.zeros(E) if bias is None else bias.clone().float()).requires_grad_(True)
     w1 = (torch.randn(E, dff, d, generator=g) * std).requires_grad_(True)
     w2 = (torch.randn(E, d, dff, generator=g) * std).requires_grad_(True)

@@ -71,7 +71,7 @@ class MoELayer(torch.nn.Module):
     def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int = 2, *,
                  replicas=None, group=None, renorm: bool = False, seed: int = 0,
                  init_std: float = 0.02, router_bias=None, device=None, exchange: str | None = None,
-                 activation: str = "gelu"):
+                 activation: str = "gelu", router_std: float | None = None):
         super().__init__()
         if activation not in ("gelu", "swiglu"):
             raise ValueError("activation must be 'gelu' (GPT MLP) or 'swiglu' (Mixtral)")
@@ -91,7 +91,8 @@ class MoELayer(torch.nn.Module):
         g = torch.Generator(device=dev)
         g.manual_seed(seed)
         self.wg = torch.nn.Parameter(
-            (torch.randn(n_experts, d_model, generator=g, device=dev) * init_std).bfloat16())
+            (torch.randn(n_experts, d_model, generator=g, device=dev) *
+             (init_std if router_std is None else router_std)).bfloat16())
         bias = torch.zeros(n_experts, device=dev) if router_bias is None else \
             torch.as_tensor(router_bias, dtype=torch.float32, device=dev)
         self.bg = torch.nn.Parameter(bias.float().clone())
