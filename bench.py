@@ -211,6 +211,7 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     layer.check()
     imbalance = layer.imbalance()
+    rows_local = int(layer.last_plan.recv_m.sum())  # assignments this rank's experts process
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -359,7 +360,8 @@ def run_gpu(args, cfg):
         P = Tn * k
         gemms_per_step = 6 if cfg["bwd"] else 2
         n_mat = 3 if act == "swiglu" else 2
-        flops_per_step = 2.0 * P * d * dff * n_mat * (3 if cfg["bwd"] else 1)
+        # algorithmic FLOPs of this rank's expert GEMMs (rows it received; = P at N = 1)
+        flops_per_step = 2.0 * rows_local * d * dff * n_mat * (3 if cfg["bwd"] else 1)
         flops_per_launch = flops_per_step / gemms_per_step
         achieved = flops_per_step * args.steps / (gemm_ms * 1e-3) / 1e12
         traffic = None
