@@ -117,12 +117,15 @@ class ReplicaGroups:
         if self.n == 1:
             return
         for pg, pos in self.buckets(local_ids):
-            # maximal runs of consecutive local positions: in-place views, no copies
-            runs, a = [], pos[0]
-            for x, y in zip(pos, pos[1:] + [None]):
-                if y != x + 1:
-                    runs.append((a, x + 1))
-                    a = y
+            # runs of consecutive EXPERT IDS: every member rank hosts all of them, so they
+            # are contiguous local positions on every member and all members issue the same
+            # sequence of equally sized in-place all-reduces (no copies)
+            ids = [local_ids[p] for p in pos]
+            runs, a = [], 0
+            for i in range(1, len(ids) + 1):
+                if i == len(ids) or ids[i] != ids[i - 1] + 1:
+                    runs.append((pos[a], pos[i - 1] + 1))
+                    a = i
             for g in grads:
                 for a, b in runs:
                     dist.all_reduce(g[a:b], group=pg)

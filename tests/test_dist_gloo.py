@@ -31,7 +31,7 @@ def _worker(rank, n, port, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=n)
     try:
-        E, k, d, P_tok = 6, 2, 8, 40
+        E, k, d, P_tok = 6, 2, 8, 40  # noqa: F841
         rng = np.random.default_rng(100 + rank)
         routed = rng.choice(E, size=P_tok * k, p=np.array([.4, .2, .15, .1, .1, .05])).astype(np.int32)
         hist = torch.from_numpy(np.bincount(routed, minlength=E).astype(np.int32))
@@ -73,7 +73,10 @@ def _worker(rank, n, port, q):
                 toks = idx_i[base + pre: base + pre + c] // k
                 want = torch.from_numpy(toks).float().repeat_interleave(d).view(c, d) + 1000 * i
                 assert torch.equal(X[src_off[e][i]:src_off[e][i] + c], want)
-        # (4) replica-group all-reduce in place (experts sharing an owner set share a group)
+        # (4) replica-group all-reduce in place (experts sharing an owner set share a group);
+        # a hand-made R where the same owner set maps to different local positions per rank
+        if n == 3:
+            R = [[1, 1, 0], [0, 1, 1], [1, 1, 0], [1, 0, 1], [1, 1, 0], [0, 1, 1]]
         groups = comm.ReplicaGroups(R)
         local = [e for e in range(E) if R[e][rank] > 0]
         g1 = torch.stack([torch.full((3, 2), float(rank + 1) * (e + 1)) for e in local])
