@@ -114,8 +114,15 @@ class ReplicaGroups:
     def allreduce(self, grads: Sequence[torch.Tensor], local_ids: Sequence[int]) -> None:
         """Sum each local expert's gradient slices ([E_loc, ...] tensors) over the
         expert's owner ranks, in place."""
+        for w in self.allreduce_async(grads, local_ids):
+            w.wait()
+
+    def allreduce_async(self, grads: Sequence[torch.Tensor], local_ids: Sequence[int]) -> list:
+        """As :meth:`allreduce`, issued asynchronously (NCCL streams); returns the works
+        whose ``wait()`` makes the current stream wait for the sums."""
+        works: list = []
         if self.n == 1:
-            return
+            return works
         for pg, pos in self.buckets(local_ids):
             # runs of consecutive EXPERT IDS: every member rank hosts all of them, so they
             # are contiguous local positions on every member and all members issue the same
@@ -128,4 +135,5 @@ class ReplicaGroups:
                     a = i
             for g in grads:
                 for a, b in runs:
-                    dist.all_reduce(g[a:b], group=pg)
+                    works.append(dist.all_reduce(g[a:b], group=pg, async_op=True))
+        return works

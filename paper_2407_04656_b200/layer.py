@@ -104,6 +104,8 @@ class MoELayer(torch.nn.Module):
         self._symm_group = None
         self._fwd_version = 0
         self.stage_events: list | None = None
+        # SMs the backward GEMMs leave to NCCL while the expert-gradient all-reduce runs
+        self.overlap_reserve = int(os.environ.get("LZ_OVERLAP_SMS", "16"))
         self.set_plan(replicas)
 
     # ------------------------------------------------------------- plan
@@ -185,6 +187,10 @@ class MoELayer(torch.nn.Module):
             return float("nan")
         recv = p.D.sum(dim=(0, 1)).float()
         return float(recv.max() / recv.mean().clamp_min(1))
+
+
+def lzh_num_sms() -> int:
+    return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
 def _mark(layer, name: str) -> None:
@@ -341,15 +347,25 @@ class _MoEFunction(torch.autograd.Function):
         dH = torch.empty_like(H)
         dW1 = torch.empty_like(w1)
         dW2 = torch.empty_like(w2)
+        works = []
+        # while the replica-group all-reduces of the weight gradients run on NCCL's
+        # streams, the remaining GEMMs leave `overlap_reserve` SMs free for them
+        ov = max(2, (lzh_num_sms() - layer.overlap_reserve)) if N > 1 else 0
         if G > 0:
             # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H)
             ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
                                   epilogue=_lib.LZ_EPI_DSWIGLU if swi else _lib.LZ_EPI_DGELU)
-            # dX = dH . W1 (W1_e [d_ff, d] read MN-major)
-            ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR)
-            # variable-K weight gradients: dW1_e = dH_e^T X_e, dW2_e = dY_e^T A_e
-            ops.grouped_gemm_wgrad(dH, X, off, dW1)
+            # variable-K weight gradients: dW2_e = dY_e^T A_e, dW1_e = dH_e^T X_e
             ops.grouped_gemm_wgrad(dY, A, off, dW2)
+        if N > 1:
+            works += layer.replica_groups.allreduce_async([dW2], layer.local_ids)
+        if G > 0:
+            ops.grouped_gemm_wgrad(dH, X, off, dW1, num_sms=ov)
+        if N > 1:
+            works += layer.replica_groups.allreduce_async([dW1], layer.local_ids)
+        if G > 0:
+            # dX = dH . W1 (W1_e [d_ff, d] read MN-major)
+            ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR, num_sms=ov)
         _mark(layer, "ffn_bwd")
         if mode == "local":
             dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
@@ -369,7 +385,8 @@ class _MoEFunction(torch.autograd.Function):
         dwg, dbg = ops.router_wgrad(dlog, x)
         _mark(layer, "router_wgrad")
         if N > 1:
-            layer.replica_groups.allreduce([dW1, dW2], layer.local_ids)
+            for wk in works:
+                wk.wait()
             flat = torch.cat([dwg.view(-1), dbg])
             dist.all_reduce(flat, group=group)
             dwg = flat[:dwg.numel()].view_as(dwg)
