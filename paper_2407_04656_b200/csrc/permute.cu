@@ -179,29 +179,33 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
   }
 }
 
-// Gate backward (softmax + top-k (+renorm)) and dispatch backward.  A warp owns a
-// group of kTG tokens: it first computes their dlogits (lane = expert), then sweeps the
-// row in 16-byte chunks accumulating sum_s dxe[row(t,s)] + dlogits[t,:] . wg for all kTG
-// tokens at once, so each wg chunk is read from L1 once per kTG tokens.
-constexpr int kTG = 8;
+// Gate backward (softmax + top-k (+renorm)) and dispatch backward.  A warp owns 16
+// tokens.  Phase A computes their dlogits (lane = expert) into smem; phase B sweeps the
+// row 64 columns at a time as a register-tiled 16 x 64 x E product (lane = 4 tokens x 8
+// columns, one 16-byte wg load feeds 32 FMAs) plus the gathered expert rows
+// sum_s dxe[row(t, s)], stored with 128-byte coalesced rows.
+constexpr int kDT = 16;
 __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
     const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
     int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
-    const float* __restrict__ dwv, const uint4* __restrict__ wg, int E, int renorm,
+    const float* __restrict__ dwv, const __nv_bfloat16* __restrict__ wg, int E, int renorm,
     uint4* __restrict__ dx, float* __restrict__ dlogits) {
-  __shared__ float s_dl[kRowWarps][kTG][64];
-  __shared__ long long s_src[kRowWarps][kTG][LZ_MAX_TOPK];  // row base address per (token, s)
+  __shared__ __align__(16) float s_dl[kRowWarps][64][kDT];        // [expert][token]
+  __shared__ long long s_src[kRowWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const long gw = (long)blockIdx.x * kRowWarps + warp;
   const long nw = (long)gridDim.x * kRowWarps;
   const int nch = d / 8;
-  for (long t0 = gw * kTG; t0 < Tn; t0 += nw * kTG) {
-    for (int ti = 0; ti < kTG; ++ti) {
+  const int tq = lane >> 3;        // token quad: tokens 4*tq .. 4*tq+3
+  const int cq = lane & 7;         // 16-byte column chunk inside the 64-column pass
+  for (long t0 = gw * kDT; t0 < Tn; t0 += nw * kDT) {
+    // ---- phase A: dlogits of the 16 tokens ------------------------------------
+    for (int ti = 0; ti < kDT; ++ti) {
       const long t = t0 + ti;
       if (t >= Tn) {
-        s_dl[warp][ti][lane] = 0.f;
-        s_dl[warp][ti][lane + 32] = 0.f;
+        s_dl[warp][lane][ti] = 0.f;
+        s_dl[warp][lane + 32][ti] = 0.f;
         continue;
       }
       const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
@@ -212,7 +216,6 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
         const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[my_rk]) : dxe;
         s_src[warp][ti][lane] = (long long)(base + (long)my_row * nch);
       }
-      // lane owns experts e = lane and e = lane + 32 (E <= 64)
       float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
@@ -244,43 +247,45 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
       for (int h = 0; h < 2; ++h) {
         const int e = lane + 32 * h;
         const float dl = p[h] * (dp[h] - pdp);
-        s_dl[warp][ti][e] = dl;
+        s_dl[warp][e][ti] = dl;
         if (e < E) dlogits[t * E + e] = dl;
       }
     }
     __syncwarp();
-    const int nt = (int)min((long)kTG, Tn - t0);
-    for (int c = lane; c < nch; c += 32) {
-      float acc[kTG][8];
+    const int nt = (int)min((long)kDT, Tn - t0);
+    // ---- phase B: dx rows, 64 columns per pass -----------------------------------
+    for (int c = cq; c < nch; c += 8) {
+      float acc[4][8];
 #pragma unroll
-      for (int ti = 0; ti < kTG; ++ti) {
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) acc[ti][q] = 0.f;
+        for (int q = 0; q < 8; ++q) acc[i][q] = 0.f;
+      if (wg) {
+        for (int e = 0; e < E; ++e) {
+          float w[8];
+          bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wg + (long)e * d) + c), w);
+          const float4 dl4 = *reinterpret_cast<const float4*>(&s_dl[warp][e][4 * tq]);
+          const float dlv[4] = {dl4.x, dl4.y, dl4.z, dl4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[i][q] = fmaf(dlv[i], w[q], acc[i][q]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int ti = 4 * tq + i;
         if (ti < nt) {
           for (int s2 = 0; s2 < k; ++s2) {
             const uint4* src = reinterpret_cast<const uint4*>(s_src[warp][ti][s2]);
             float f[8];
             bf16x8_to_f32(ld_nc_v4(src + c), f);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[ti][q] += f[q];
+            for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
           }
+          st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(acc[i]));
         }
       }
-      if (wg) {
-        for (int e = 0; e < E; ++e) {
-          float f[8];
-          bf16x8_to_f32(__ldg(wg + (long)e * nch + c), f);
-#pragma unroll
-          for (int ti = 0; ti < kTG; ++ti) {
-            const float de = s_dl[warp][ti][e];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) acc[ti][q] = fmaf(de, f[q], acc[ti][q]);
-          }
-        }
-      }
-#pragma unroll
-      for (int ti = 0; ti < kTG; ++ti)
-        if (ti < nt) st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(acc[ti]));
     }
     __syncwarp();
   }
@@ -370,20 +375,30 @@ __global__ void __launch_bounds__(256, 2) router_wgrad_partial(const float* __re
     part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
 }
 
-__global__ void router_wgrad_reduce(const float* __restrict__ part,
-                                    const float* __restrict__ part_bias, int nblk, int d, int E,
-                                    float* __restrict__ dwg, float* __restrict__ dbias) {
-  const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+// 16 lanes per output element, each summing a strided subset of the block partials,
+// then a 16-lane shuffle reduction (fixed order: deterministic).
+__global__ void __launch_bounds__(256) router_wgrad_reduce(const float* __restrict__ part,
+                                                           const float* __restrict__ part_bias,
+                                                           int nblk, int d, int E,
+                                                           float* __restrict__ dwg,
+                                                           float* __restrict__ dbias) {
   const long n = (long)E * d;
-  if (i < n) {
-    float s = 0.f;
-    for (int b = 0; b < nblk; ++b) s += part[(long)b * n + i];
-    dwg[i] = s;
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long i = gid >> 4;
+  const int sub = threadIdx.x & 15;
+  float s = 0.f, sb = 0.f;
+  if (i < n)
+    for (int b = sub; b < nblk; b += 16) s += part[(long)b * n + i];
+  if (dbias && i < E)
+    for (int b = sub; b < nblk; b += 16) sb += part_bias[(long)b * E + i];
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    sb += __shfl_xor_sync(0xffffffffu, sb, o);
   }
-  if (dbias && i < E) {
-    float s = 0.f;
-    for (int b = 0; b < nblk; ++b) s += part_bias[(long)b * E + i];
-    dbias[i] = s;
+  if (sub == 0 && i < n) {
+    dwg[i] = s;
+    if (dbias && i < E) dbias[i] = sb;
   }
 }
 
@@ -518,9 +533,10 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
     return LZ_ERR_ARG;
   if (Tn == 0) return LZ_OK;
   if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
-  dispatch_bwd_kernel<<<row_grid((Tn + kTG - 1) / kTG), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const uint4*)wg, E, renorm,
-      (uint4*)dx, dlogits);
+  if (d % 64) return LZ_ERR_UNSUPPORTED;
+  dispatch_bwd_kernel<<<row_grid((Tn + kDT - 1) / kDT), kRowThreads, 0, (cudaStream_t)stream>>>(
+      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const __nv_bfloat16*)wg, E,
+      renorm, (uint4*)dx, dlogits);
   return lzh::check_launch();
 }
 
@@ -576,8 +592,8 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
   lz_status st = lzh::check_launch();
   if (st != LZ_OK) return st;
   const long n = (long)E * d;
-  router_wgrad_reduce<<<(int)((n + 255) / 256), 256, 0, s>>>(part, part_bias, nblk, d, E, dwg,
-                                                             dbias);
+  router_wgrad_reduce<<<(int)((16 * n + 255) / 256), 256, 0, s>>>(part, part_bias, nblk, d, E,
+                                                                  dwg, dbias);
   return lzh::check_launch();
 }
 
