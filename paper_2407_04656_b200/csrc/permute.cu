@@ -255,6 +255,21 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
     const int nt = (int)min((long)kDT, Tn - t0);
     // ---- phase B: dx rows, 64 columns per pass -----------------------------------
     for (int c = cq; c < nch; c += 8) {
+      // issue the gathered expert-row loads first (k <= 2 fast path); the E-long FMA
+      // loop below hides their latency
+      uint4 pre[4][2];
+      const bool fast = k <= 2;
+      if (fast) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int ti = 4 * tq + i;
+#pragma unroll
+          for (int s2 = 0; s2 < 2; ++s2)
+            pre[i][s2] = (ti < nt && s2 < k)
+                             ? ld_nc_v4(reinterpret_cast<const uint4*>(s_src[warp][ti][s2]) + c)
+                             : make_uint4(0, 0, 0, 0);
+        }
+      }
       float acc[4][8];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
@@ -276,12 +291,22 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
       for (int i = 0; i < 4; ++i) {
         const int ti = 4 * tq + i;
         if (ti < nt) {
-          for (int s2 = 0; s2 < k; ++s2) {
-            const uint4* src = reinterpret_cast<const uint4*>(s_src[warp][ti][s2]);
-            float f[8];
-            bf16x8_to_f32(ld_nc_v4(src + c), f);
+          if (fast) {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
+            for (int s2 = 0; s2 < 2; ++s2) {
+              float f[8];
+              bf16x8_to_f32(pre[i][s2], f);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
+            }
+          } else {
+            for (int s2 = 0; s2 < k; ++s2) {
+              const uint4* src = reinterpret_cast<const uint4*>(s_src[warp][ti][s2]);
+              float f[8];
+              bf16x8_to_f32(ld_nc_v4(src + c), f);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
+            }
           }
           st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(acc[i]));
         }
