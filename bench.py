@@ -38,6 +38,8 @@ CONFIGS = {
                  act="swiglu", cpu_tokens=256, cpu_reps=1,
                  name="Mixtral-8x7B-shape MoE layer (E8 top-2 d4096 d_ff14336 SwiGLU, 16K tok/GPU, "
                       "fwd+bwd + replica-group grad all-reduce)"),
+    "cfg5": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=5, bwd=True,
+                 name="elastic reconfiguration 8->6->4 (cfg2 shape, slots held at the 8-GPU value)"),
     "cfg4": dict(E=64, k=1, d=2048, dff=None, tokens=131072, s=1.5, slot_factor=4, bwd=False,
                  name="E64 top-1 d2048 dispatch/combine-only sweep (8K..1M tok/GPU, Zipf 1.5)"),
 }
@@ -513,6 +515,90 @@ def run_dispatch_sweep(args, cfg):
     return 0
 
 
+def run_elastic(args, cfg):
+    """Config 5: measure the layer on N ranks, remove ranks twice (8 -> 6 -> 4 on 8 GPUs,
+    4 -> 3 -> 2 on 4), re-plan on the host with the reference recipe, migrate expert state
+    over NVLink, and measure again on the survivors with the SAME kernels.  Slots per GPU
+    stay at the full-size value (slots are per-GPU memory)."""
+    import torch.distributed as dist
+
+    from paper_2407_04656_b200 import ops
+    from paper_2407_04656_b200.elastic import shrink_and_replan
+    from paper_2407_04656_b200.layer import MoELayer, zipf_router_bias
+    from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix
+
+    rank, world, local = _env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    E, k, d, dff, Tn = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["tokens"]
+    c = math.ceil(cfg["slot_factor"] * E / world)
+    bias = zipf_router_bias(E, cfg["s"], seed=0)
+    layer = MoELayer(d, dff, E, k, seed=0, router_bias=bias, device=dev,
+                     router_std=1.28 / math.sqrt(d), group=dist.group.WORLD)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+    x = torch.randn(Tn, d, generator=g, device=dev).bfloat16()
+    dout = (torch.randn(Tn, d, generator=g, device=dev) * 1e-2).bfloat16()
+    hist = ops.router_gate(x, layer.wg.detach(), layer.bg.detach(), k)[3].long()
+    dist.all_reduce(hist)
+    loads = hist.cpu().tolist()
+    layer.set_plan(replica_matrix(plan_for_loads(loads, world, c, 2)))
+    group = dist.group.WORLD
+
+    def measure(grp):
+        for _ in range(max(args.warmup, 3)):
+            layer.zero_grad(set_to_none=True)
+            layer(x).backward(dout)
+        torch.cuda.synchronize()
+        dist.barrier(group=grp)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            layer.zero_grad(set_to_none=True)
+            layer(x).backward(dout)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=grp)
+        n = dist.get_world_size(grp)
+        ms = float(t.item()) / args.steps
+        return {"n_gpus": n, "ms_per_step": ms, "tokens_per_s": n * Tn / (ms * 1e-3),
+                "tokens_per_s_per_gpu": Tn / (ms * 1e-3), "imbalance": round(layer.imbalance(), 4)}
+
+    phases = [measure(group)]
+    # two failure events; never remove rank 0 (it reports)
+    drops = ([3, 6], [1, 4]) if world == 8 else ([world - 1], [world - 2]) if world >= 4 else ()
+    reconf = []
+    for ex in drops:
+        if dist.get_rank(group) in ex:
+            os._exit(0)  # this rank "fails"
+        t0 = time.perf_counter()
+        layer, group, rep = shrink_and_replan(layer, group, ex, loads, c)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        reconf.append({"excluded": ex, "seconds": round(dt, 3), "transfers": rep["transfers"],
+                       "bytes": rep["bytes"], "checkpoint_fallback": len(rep["checkpoint_fallback"]),
+                       "replicas": rep["replicas"]})
+        phases.append(measure(group))
+    if dist.get_rank(group) == 0:
+        base = phases[0]["tokens_per_s_per_gpu"]
+        for ph in phases:
+            ph["retained_per_gpu_vs_full"] = round(ph["tokens_per_s_per_gpu"] / base, 4)
+        last = phases[-1]
+        line = {"metric": METRIC + " on survivors after elastic reconfiguration",
+                "value": last["tokens_per_s"], "unit": "tokens/s", "n_gpus": last["n_gpus"],
+                "steps": args.steps, "warmup": max(args.warmup, 3),
+                "ms_per_step": last["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+                "config": {"workload": cfg["name"], "slots_per_gpu": c, "start_gpus": world},
+                "phases": phases, "reconfigurations": reconf}
+        print(json.dumps(line), flush=True)
+    dist.barrier(group=group)
+    dist.destroy_process_group()
+    return 0
+
+
 def plan_replicas(plan, E):
     counts = [0] * E
     for row in plan.slots:
@@ -537,6 +623,8 @@ def main():
         return run_reference(args, cfg)
     if args.config == "cfg4":
         return run_dispatch_sweep(args, cfg)
+    if args.config == "cfg5":
+        return run_elastic(args, cfg)
     return run_gpu(args, cfg)
 
 
