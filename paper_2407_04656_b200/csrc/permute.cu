@@ -180,83 +180,105 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
 }
 
 // Gate backward (softmax + top-k (+renorm)) and dispatch backward.  A warp owns 16
-// tokens.  Phase A computes their dlogits (lane = expert) into smem; phase B sweeps the
-// row 64 columns at a time as a register-tiled 16 x 64 x E product (lane = 4 tokens x 8
-// columns, one 16-byte wg load feeds 32 FMAs) plus the gathered expert rows
-// sum_s dxe[row(t, s)], stored with 128-byte coalesced rows.
+// tokens.  Phase A computes their dlogits (lane = expert) into smem.  Phase B sweeps the
+// row 64 columns at a time: the router term dlogits[16 x E] . wg[E x 64] runs on the
+// tensor cores (mma.sync m16n8k16, dlogits split into bf16 hi + lo so the product keeps
+// ~16 mantissa bits), is staged through smem, and joins the gathered expert rows
+// sum_s dxe[row(t, s)] in a 128-byte coalesced row pass.
 constexpr int kDT = 16;
-__global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
+constexpr int kDWarps = 4;
+__device__ __forceinline__ uint32_t bf16pair(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+template <int KS>
+__global__ void __launch_bounds__(32 * kDWarps) dispatch_bwd_kernel(
     const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
     int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
     const float* __restrict__ dwv, const __nv_bfloat16* __restrict__ wg, int E, int renorm,
     uint4* __restrict__ dx, float* __restrict__ dlogits) {
-  __shared__ __align__(16) float s_dl[kRowWarps][64][kDT];        // [expert][token]
-  __shared__ long long s_src[kRowWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
+  __shared__ __align__(16) float s_dl[kDWarps][64][kDT + 1];    // [expert][token]
+  __shared__ __align__(16) float s_rt[kDWarps][kDT][64 + 4];    // router term, one pass
+  __shared__ long long s_src[kDWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  const long gw = (long)blockIdx.x * kRowWarps + warp;
-  const long nw = (long)gridDim.x * kRowWarps;
+  const long gw = (long)blockIdx.x * kDWarps + warp;
+  const long nw = (long)gridDim.x * kDWarps;
   const int nch = d / 8;
-  const int tq = lane >> 3;        // token quad: tokens 4*tq .. 4*tq+3
-  const int cq = lane & 7;         // 16-byte column chunk inside the 64-column pass
+  const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  const int tq = lane >> 3;                 // row pass: tokens 4*tq .. 4*tq+3
+  const int cq = lane & 7;                  // row pass: 16-byte chunk inside the 64 columns
   for (long t0 = gw * kDT; t0 < Tn; t0 += nw * kDT) {
-    // ---- phase A: dlogits of the 16 tokens ------------------------------------
-    for (int ti = 0; ti < kDT; ++ti) {
+    // ---- phase A: dlogits, one lane per token (lanes 0..15) ----------------------
+    // dp_e is non-zero only at the k routed experts, so
+    //   dot = sum_s g_s p_{idx_s},  dl_e = p_e (dp_e - dot)
+    // with g_s = dw_s (renorm: (dw_s - sum_s' dw_s' w_s') / S, S = sum_s p_{idx_s}).
+    if (lane < kDT) {
+      const int ti = lane;
       const long t = t0 + ti;
-      if (t >= Tn) {
-        s_dl[warp][lane][ti] = 0.f;
-        s_dl[warp][lane + 32][ti] = 0.f;
-        continue;
-      }
-      const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
-      const int my_idx = lane < k ? __ldg(idx + t * k + lane) : -1;
-      const float my_dw = lane < k ? __ldg(dwv + t * k + lane) : 0.f;
-      const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
-      if (lane < k) {
-        const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[my_rk]) : dxe;
-        s_src[warp][ti][lane] = (long long)(base + (long)my_row * nch);
-      }
-      float p[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = lane + 32 * h;
-        if (e < E) p[h] = __ldg(probs + t * E + e);
-      }
-      float S = 0.f, sum_dw_w = 0.f;
-      if (renorm) {
+      if (t < Tn) {
+        int ids[LZ_MAX_TOPK];
+        float gs[LZ_MAX_TOPK], ps[LZ_MAX_TOPK];
+        float S = 0.f, sdw = 0.f;
         for (int s2 = 0; s2 < k; ++s2) {
-          const int es = __shfl_sync(0xffffffffu, my_idx, s2);
-          S += __ldg(probs + t * E + es);
+          const int e = __ldg(idx + t * k + s2);
+          ids[s2] = e;
+          gs[s2] = __ldg(dwv + t * k + s2);
+          ps[s2] = __ldg(probs + t * E + e);
+          S += ps[s2];
+          const int rr = __ldg(row + t * k + s2);
+          const int rk = peers ? __ldg(prank + t * k + s2) : 0;
+          const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[rk]) : dxe;
+          s_src[warp][ti][s2] = (long long)(base + (long)rr * nch);
         }
-        for (int s2 = 0; s2 < k; ++s2) {
-          const int es = __shfl_sync(0xffffffffu, my_idx, s2);
-          const float dws = __shfl_sync(0xffffffffu, my_dw, s2);
-          sum_dw_w += dws * (__ldg(probs + t * E + es) / S);
+        if (renorm) {
+          for (int s2 = 0; s2 < k; ++s2) sdw += gs[s2] * (ps[s2] / S);
+          for (int s2 = 0; s2 < k; ++s2) gs[s2] = (gs[s2] - sdw) / S;
         }
-      }
-      for (int s2 = 0; s2 < k; ++s2) {
-        const int es = __shfl_sync(0xffffffffu, my_idx, s2);
-        const float dws = __shfl_sync(0xffffffffu, my_dw, s2);
-        const float g = renorm ? (dws - sum_dw_w) / S : dws;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (es == lane + 32 * h) dp[h] += g;
-      }
-      const float pdp = warp_sum(p[0] * dp[0] + p[1] * dp[1]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = lane + 32 * h;
-        const float dl = p[h] * (dp[h] - pdp);
-        s_dl[warp][e][ti] = dl;
-        if (e < E) dlogits[t * E + e] = dl;
+        float dot = 0.f;
+        for (int s2 = 0; s2 < k; ++s2) dot += gs[s2] * ps[s2];
+        for (int e = 0; e < 64; ++e) s_dl[warp][e][ti] = 0.f;
+        for (int e = 0; e < E; ++e) s_dl[warp][e][ti] = -__ldg(probs + t * E + e) * dot;
+        for (int s2 = 0; s2 < k; ++s2) s_dl[warp][ids[s2]][ti] += ps[s2] * gs[s2];
+        for (int e = 0; e < E; ++e) dlogits[t * E + e] = s_dl[warp][e][ti];
+      } else {
+        for (int e = 0; e < 64; ++e) s_dl[warp][e][ti] = 0.f;
       }
     }
     __syncwarp();
     const int nt = (int)min((long)kDT, Tn - t0);
-    // ---- phase B: dx rows, 64 columns per pass -----------------------------------
-    for (int c = cq; c < nch; c += 8) {
-      // issue the gathered expert-row loads first (k <= 2 fast path); the E-long FMA
-      // loop below hides their latency
+    // A fragments (dlogits as hi + lo bf16), per 16-expert k step (E <= 64)
+    uint32_t ah[KS][4], al[KS][4];
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      {
+        const int e0 = ks * 16 + 2 * t4;
+        const float v[8] = {s_dl[warp][e0][g],     s_dl[warp][e0 + 1][g],
+                            s_dl[warp][e0][g + 8], s_dl[warp][e0 + 1][g + 8],
+                            s_dl[warp][e0 + 8][g], s_dl[warp][e0 + 9][g],
+                            s_dl[warp][e0 + 8][g + 8], s_dl[warp][e0 + 9][g + 8]};
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float x0 = v[2 * r], x1 = v[2 * r + 1];
+          ah[ks][r] = bf16pair(x0, x1);
+          const float h0 = __uint_as_float(ah[ks][r] << 16);
+          const float h1 = __uint_as_float(ah[ks][r] & 0xffff0000u);
+          al[ks][r] = bf16pair(x0 - h0, x1 - h1);
+        }
+      }
+    }
+    // ---- phase B: 64 columns per pass -----------------------------------------
+    for (int c0 = 0; c0 < d; c0 += 64) {
+      // issue the gathered expert-row loads first (k <= 2 fast path)
+      const int c = (c0 >> 3) + cq;
       uint4 pre[4][2];
       const bool fast = k <= 2;
       if (fast) {
@@ -270,26 +292,57 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
                              : make_uint4(0, 0, 0, 0);
         }
       }
-      float acc[4][8];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[i][q] = 0.f;
       if (wg) {
-        for (int e = 0; e < E; ++e) {
-          float w[8];
-          bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(wg + (long)e * d) + c), w);
-          const float4 dl4 = *reinterpret_cast<const float4*>(&s_dl[warp][e][4 * tq]);
-          const float dlv[4] = {dl4.x, dl4.y, dl4.z, dl4.w};
+        float acc[8][4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+        for (int n8 = 0; n8 < 8; ++n8)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[i][q] = fmaf(dlv[i], w[q], acc[i][q]);
+          for (int q = 0; q < 4; ++q) acc[n8][q] = 0.f;
+        const unsigned short* wbase = reinterpret_cast<const unsigned short*>(wg) + c0 + g;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          {
+            // all 32 weight loads of this k step first, then 16 MMAs (hi + lo)
+            const int e0 = ks * 16 + 2 * t4;
+            uint32_t w[8][4];
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int e = e0 + (j & 1) + (j >> 1) * 8;
+                w[n8][j] = e < E ? (uint32_t)__ldg(wbase + (long)e * d + n8 * 8) : 0u;
+              }
+#pragma unroll
+            for (int n8 = 0; n8 < 8; ++n8) {
+              const uint32_t b0 = w[n8][0] | (w[n8][1] << 16);
+              const uint32_t b1 = w[n8][2] | (w[n8][3] << 16);
+              mma16816(acc[n8], ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], b0, b1);
+              mma16816(acc[n8], al[ks][0], al[ks][1], al[ks][2], al[ks][3], b0, b1);
+            }
+          }
+        }
+#pragma unroll
+        for (int n8 = 0; n8 < 8; ++n8) {
+          s_rt[warp][g][n8 * 8 + 2 * t4] = acc[n8][0];
+          s_rt[warp][g][n8 * 8 + 2 * t4 + 1] = acc[n8][1];
+          s_rt[warp][g + 8][n8 * 8 + 2 * t4] = acc[n8][2];
+          s_rt[warp][g + 8][n8 * 8 + 2 * t4 + 1] = acc[n8][3];
         }
       }
+      __syncwarp();
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int ti = 4 * tq + i;
+        float f8[8];
+        if (wg) {
+          const float4 r0 = *reinterpret_cast<const float4*>(&s_rt[warp][ti][cq * 8]);
+          const float4 r1 = *reinterpret_cast<const float4*>(&s_rt[warp][ti][cq * 8 + 4]);
+          f8[0] = r0.x; f8[1] = r0.y; f8[2] = r0.z; f8[3] = r0.w;
+          f8[4] = r1.x; f8[5] = r1.y; f8[6] = r1.z; f8[7] = r1.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) f8[q] = 0.f;
+        }
         if (ti < nt) {
           if (fast) {
 #pragma unroll
@@ -297,7 +350,7 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
               float f[8];
               bf16x8_to_f32(pre[i][s2], f);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
+              for (int q = 0; q < 8; ++q) f8[q] += f[q];
             }
           } else {
             for (int s2 = 0; s2 < k; ++s2) {
@@ -305,14 +358,14 @@ __global__ void __launch_bounds__(kRowThreads) dispatch_bwd_kernel(
               float f[8];
               bf16x8_to_f32(ld_nc_v4(src + c), f);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc[i][q] += f[q];
+              for (int q = 0; q < 8; ++q) f8[q] += f[q];
             }
           }
-          st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(acc[i]));
+          st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(f8));
         }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
@@ -559,9 +612,21 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
   if (Tn == 0) return LZ_OK;
   if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
   if (d % 64) return LZ_ERR_UNSUPPORTED;
-  dispatch_bwd_kernel<<<row_grid((Tn + kDT - 1) / kDT), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const __nv_bfloat16*)wg, E,
-      renorm, (uint4*)dx, dlogits);
+  const long dtasks = (Tn + kDT - 1) / kDT;
+  long dgrid = (dtasks + kDWarps - 1) / kDWarps;
+  const long dcap = (long)lzh::num_sms() * 16;
+  if (dgrid > dcap) dgrid = dcap;
+#define LZ_DBWD(ks)                                                                          \
+  dispatch_bwd_kernel<ks><<<(int)dgrid, 32 * kDWarps, 0, (cudaStream_t)stream>>>(              \
+      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const __nv_bfloat16*)wg, \
+      E, renorm, (uint4*)dx, dlogits)
+  switch ((E + 15) / 16) {
+    case 1: LZ_DBWD(1); break;
+    case 2: LZ_DBWD(2); break;
+    case 3: LZ_DBWD(3); break;
+    default: LZ_DBWD(4); break;
+  }
+#undef LZ_DBWD
   return lzh::check_launch();
 }
 
