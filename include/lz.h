@@ -168,10 +168,11 @@ lz_status lz_combine_bwd(const void* dout, const void* y, const int32_t* row, co
 
 /* Gate backward + dispatch backward, fused per token:
  *   dlogits[t,:] from probs, idx, dw (softmax/top-k(/renorm) backward)
- *   dx[t] = sum_s dxe[row[t,s]] + dlogits[t,:] . wg        (wg bf16 [E, d]; may be NULL) */
+ *   dx[t] = sum_s dxe[row[t,s]] + dlogits[t,:] . wg
+ * wgT is the router weight TRANSPOSED, bf16 [d, E] (E even; may be NULL); d % 64 == 0. */
 lz_status lz_dispatch_bwd(const void* dxe, const int32_t* row, int Tn, int d, int k,
                           const float* probs, const int32_t* idx, const float* dw,
-                          const void* wg, int E, int renorm, void* dx, float* dlogits,
+                          const void* wgT, int E, int renorm, void* dx, float* dlogits,
                           void* stream);
 
 /* Router weight gradient: dwg[E, d] (fp32) = dlogits^T . x ; dbias[E] = sum_t dlogits.

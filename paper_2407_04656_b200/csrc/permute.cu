@@ -298,27 +298,23 @@ __global__ void __launch_bounds__(32 * kDWarps) dispatch_bwd_kernel(
         for (int n8 = 0; n8 < 8; ++n8)
 #pragma unroll
           for (int q = 0; q < 4; ++q) acc[n8][q] = 0.f;
-        const unsigned short* wbase = reinterpret_cast<const unsigned short*>(wg) + c0 + g;
+        // wg is passed TRANSPOSED ([d, E], experts contiguous): each B register is one
+        // 4-byte load of two consecutive experts at one column
+        const uint32_t* wT = reinterpret_cast<const uint32_t*>(wg);
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
-          {
-            // all 32 weight loads of this k step first, then 16 MMAs (hi + lo)
-            const int e0 = ks * 16 + 2 * t4;
-            uint32_t w[8][4];
+          const int e0 = ks * 16 + 2 * t4;
+          uint32_t w[8][2];
 #pragma unroll
-            for (int n8 = 0; n8 < 8; ++n8)
+          for (int n8 = 0; n8 < 8; ++n8) {
+            const long cbase = (long)(c0 + n8 * 8 + g) * E;
+            w[n8][0] = e0 < E ? __ldg(wT + ((cbase + e0) >> 1)) : 0u;
+            w[n8][1] = e0 + 8 < E ? __ldg(wT + ((cbase + e0 + 8) >> 1)) : 0u;
+          }
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int e = e0 + (j & 1) + (j >> 1) * 8;
-                w[n8][j] = e < E ? (uint32_t)__ldg(wbase + (long)e * d + n8 * 8) : 0u;
-              }
-#pragma unroll
-            for (int n8 = 0; n8 < 8; ++n8) {
-              const uint32_t b0 = w[n8][0] | (w[n8][1] << 16);
-              const uint32_t b1 = w[n8][2] | (w[n8][3] << 16);
-              mma16816(acc[n8], ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], b0, b1);
-              mma16816(acc[n8], al[ks][0], al[ks][1], al[ks][2], al[ks][3], b0, b1);
-            }
+          for (int n8 = 0; n8 < 8; ++n8) {
+            mma16816(acc[n8], ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], w[n8][0], w[n8][1]);
+            mma16816(acc[n8], al[ks][0], al[ks][1], al[ks][2], al[ks][3], w[n8][0], w[n8][1]);
           }
         }
 #pragma unroll
@@ -611,7 +607,7 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
     return LZ_ERR_ARG;
   if (Tn == 0) return LZ_OK;
   if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
-  if (d % 64) return LZ_ERR_UNSUPPORTED;
+  if (d % 64 || E % 2) return LZ_ERR_UNSUPPORTED;
   const long dtasks = (Tn + kDT - 1) / kDT;
   long dgrid = (dtasks + kDWarps - 1) / kDWarps;
   const long dcap = (long)lzh::num_sms() * 16;

@@ -114,8 +114,9 @@ def dispatch_bwd(dxe, row, probs, idx, dw, wg, renorm: bool, Tn: int):
     E = probs.shape[1]
     dx = torch.empty((Tn, d), dtype=torch.bfloat16, device=dxe.device)
     dlog = torch.empty((Tn, E), dtype=torch.float32, device=dxe.device)
+    wgT = None if wg is None else wg.t().contiguous()  # [d, E], experts contiguous
     _lib.call("lz_dispatch_bwd", ptr(dxe), ptr(row), Tn, d, k, ptr(probs), ptr(idx), ptr(dw),
-              ptr(wg), E, int(renorm), ptr(dx), ptr(dlog), _s())
+              ptr(wgT), E, int(renorm), ptr(dx), ptr(dlog), _s())
     return dx, dlog
 
 
@@ -210,8 +211,9 @@ def dispatch_bwd_p2p(peers_dxe, dest_rank, dest_row, probs, idx, dw, wg, renorm:
     E = probs.shape[1]
     dx = torch.empty((Tn, d), dtype=torch.bfloat16, device=probs.device)
     dlog = torch.empty((Tn, E), dtype=torch.float32, device=probs.device)
+    wgT = None if wg is None else wg.t().contiguous()
     _lib.call("lz_dispatch_bwd_p2p", ptr(peers_dxe), ptr(dest_rank), ptr(dest_row), Tn, d, k,
-              ptr(probs), ptr(idx), ptr(dw), ptr(wg), E, int(renorm), ptr(dx), ptr(dlog), _s())
+              ptr(probs), ptr(idx), ptr(dw), ptr(wgT), E, int(renorm), ptr(dx), ptr(dlog), _s())
     return dx, dlog
 
 
