@@ -185,12 +185,12 @@ lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, in
 
 /* Epilogues */
 #define LZ_EPI_STORE 0     /* C = acc (bf16)                                   */
-#define LZ_EPI_GELU 1      /* C = gelu(acc), AUX = acc (pre-activation, bf16)  */
-#define LZ_EPI_DGELU 2     /* C = acc * gelu'(AUX)                             */
-#define LZ_EPI_SWIGLU 3    /* B rows = W1|W3 interleaved in 128-row blocks: AUX[rows, N] = acc
-                              (gate|up pre-activations), C[rows, N/2] = silu(gate) * up */
-#define LZ_EPI_DSWIGLU 4   /* acc = dA[rows, N]; AUX = interleaved pre-activations [rows, 2N];
-                              C[rows, 2N] = [dgate | dup] interleaved like AUX            */
+#define LZ_EPI_GELU 1      /* C = gelu(acc), AUX = gelu'(acc) (bf16; the backward factor)   */
+#define LZ_EPI_DGELU 2     /* C = acc * AUX   (AUX as written by LZ_EPI_GELU)             */
+#define LZ_EPI_SWIGLU 3    /* B rows = W1|W3 interleaved in 128-row blocks; with g|u = acc:
+                              C[rows, N/2] = silu(g) * u, AUX[rows, N] = [silu(g) | u silu'(g)] */
+#define LZ_EPI_DSWIGLU 4   /* acc = dA[rows, N]; AUX = LZ_EPI_SWIGLU's [S | Q] [rows, 2N];
+                              C[rows, 2N] = [dA * Q | dA * S] = [dgate | dup]              */
 /* Operand majors */
 #define LZ_K_MAJOR 0
 #define LZ_MN_MAJOR 1

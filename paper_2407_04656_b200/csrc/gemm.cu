@@ -255,6 +255,15 @@ __device__ __forceinline__ float tanh_fast(float x) {
 }
 constexpr float kS2PI = 0.7978845608028654f;
 constexpr float kGC = 0.044715f;
+// GELU and its derivative from one tanh: the forward epilogue stores gelu'(h) (not h) as
+// the backward's aux stream, so the dGELU epilogue is a plain multiply (no MUFU in the
+// backward GEMM epilogue)
+__device__ __forceinline__ void gelu_and_grad(float x, float& y, float& dy) {
+  const float x2 = x * x;
+  const float t = tanh_fast(kS2PI * fmaf(kGC * x, x2, x));
+  y = 0.5f * x * (1.f + t);
+  dy = 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * kS2PI * fmaf(3.f * kGC, x2, 1.f);
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float u = kS2PI * fmaf(kGC * x, x * x, x);
   return 0.5f * x * (1.f + tanh_fast(u));
@@ -418,9 +427,17 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
       tma_load_2d(wbuf + 3 * kEpiBuf, map_x, abar, u2, row0);
     }
     if (fwd) {
+      // aux keeps the backward's factors, not the pre-activations:
+      //   S = silu(g) (gate column), Q = u * silu'(g) (up column); act = S * u
       float a[32];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) a[q] = g[q] * sigmoid_f(g[q]) * u[q];
+      for (int q = 0; q < 32; ++q) {
+        const float sg = sigmoid_f(g[q]);
+        const float sl = g[q] * sg;
+        a[q] = sl * u[q];
+        u[q] = u[q] * sg * (1.f + g[q] * (1.f - sg));
+        g[q] = sl;
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         st_shared_v4(s_aux0 + stg_off(lane, q), f32_to_bf16x8(g + 8 * q));
@@ -439,10 +456,9 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
       float dg[32], du[32];
 #pragma unroll
       for (int q = 0; q < 32; ++q) {
-        const float da = __uint_as_float(va[q]);
-        const float sg = sigmoid_f(g[q]);
-        du[q] = da * g[q] * sg;
-        dg[q] = da * u[q] * sg * (1.f + g[q] * (1.f - sg));
+        const float da = __uint_as_float(va[q]);  // g holds S = silu(g), u holds Q
+        du[q] = da * g[q];
+        dg[q] = da * u[q];
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -627,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
-      if (dgelu && !p.direct && lane == 0) {
+      if (dgelu && lane == 0) {
         // prefetch the first two pre-activation chunks of this tile
         fence_async_smem();
         for (int c = 0; c < 2; ++c) {
@@ -671,49 +687,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         float f[32];
 #pragma unroll
         for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-        if (p.direct == 2 && dgelu) {
-          // pre-activation read straight from global (row per thread), staged stores below
-          const __nv_bfloat16* hrow = p.aux + (long)(row0 + lane) * p.ldx + col0 + c * kEpiCols;
-          uint4 hv[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) hv[q] = ld_nc_v4(hrow + 8 * q);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float h[8];
-            bf16x8_to_f32(hv[q], h);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
-          }
-        }
-        if (p.direct == 1) {
-          // row-per-thread 16-byte stores: 4 x 16 B of this thread's row per 32 columns
-          const long grow = row0 + lane;
-          __nv_bfloat16* crow = p.C + grow * p.ldc + col0 + c * kEpiCols;
-          if (dgelu) {
-            const __nv_bfloat16* hrow = p.aux + grow * p.ldx + col0 + c * kEpiCols;
-            uint4 hv[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) hv[q] = ld_nc_v4(hrow + 8 * q);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float h[8];
-              bf16x8_to_f32(hv[q], h);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
-            }
-          }
-          if (gelu) {
-            __nv_bfloat16* xrow = p.aux + grow * p.ldx + col0 + c * kEpiCols;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) st_v4(xrow + 8 * q, f32_to_bf16x8(f + 8 * q));
-#pragma unroll
-            for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) st_v4(crow + 8 * q, f32_to_bf16x8(f + 8 * q));
-          continue;
-        }
-        if (dgelu && p.direct == 0) {
+        if (dgelu) {
+          // aux = gelu'(h) stored by the forward epilogue
           mbar_wait(&my_aux_bar[b], aux_phase[b]);
           aux_phase[b] ^= 1;
 #pragma unroll
@@ -721,24 +696,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             float h[8];
             bf16x8_to_f32(ld_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q)), h);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[8 * q + i] *= dgelu_f(h[i]);
+            for (int i = 0; i < 8; ++i) f[8 * q + i] *= h[i];
           }
         }
         // the store that used buffer b (chunk c-2) must have finished reading smem
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        if (dgelu && p.direct == 0 && c + 2 < kChunks && lane == 0) {
+        if (dgelu && c + 2 < kChunks && lane == 0) {
           fence_async_smem();
           mbar_expect_tx(&my_aux_bar[b], kEpiBuf);
           tma_load_2d(wbuf + (2 + b) * kEpiBuf, &map_x, &my_aux_bar[b],
                       col0 + (c + 2) * kEpiCols, row0);
         }
         if (gelu) {
+          float dg[32];
+#pragma unroll
+          for (int q = 0; q < 32; ++q) gelu_and_grad(f[q], f[q], dg[q]);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            st_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
-#pragma unroll
-          for (int q = 0; q < 32; ++q) f[q] = gelu_f(f[q]);
+            st_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(dg + 8 * q));
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q)
@@ -888,7 +864,7 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.epilogue = epilogue;
   p.c_grp_rows = c_group_rows > 0 ? c_group_rows : M;
   p.c_row_off = c_row_offset;
-  p.direct = epilogue <= LZ_EPI_DGELU ? g_direct_epi : 0;
+  p.direct = 0;  // register->global epilogue variants were measured 1.6-2x slower; removed
   p.C = (__nv_bfloat16*)C;
   p.aux = (__nv_bfloat16*)aux;
   p.ldc = N;
