@@ -201,6 +201,7 @@ def run_gpu(args, cfg):
     layer.set_plan(replica_matrix(plan))
 
     def step(xx, dd):
+        nonlocal layer
         layer.zero_grad(set_to_none=True)
         out = layer(xx)
         if cfg["bwd"]:
@@ -293,6 +294,21 @@ def run_gpu(args, cfg):
             t = torch.tensor([ms_graph, ms_graph_e2e], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_graph, ms_graph_e2e = (float(v) for v in t.tolist())
+        # autograd nodes created under capture stay bound to the capture stream and would
+        # force a device sync on every later eager backward: continue on a fresh layer
+        # object with identical weights and plan
+        launches_graph = graph.launches_per_step
+        del graph
+        graph = True
+        fresh = MoELayer(d, dff, E, k, seed=0, router_bias=bias, device=dev, activation=act,
+                         router_std=1.28 / math.sqrt(d), replicas=layer.R,
+                         group=None if world == 1 else dist.group.WORLD)
+        with torch.no_grad():
+            for pa, pb in zip(fresh.parameters(), layer.parameters()):
+                pa.copy_(pb)
+        layer = fresh
+        for _ in range(3):
+            step(x, dout)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -377,8 +393,7 @@ def run_gpu(args, cfg):
         eager = {"value": world * Tn * args.steps / (ms * 1e-3), "ms_per_step": ms / args.steps,
                  "e2e": world * Tn * args.steps / (ms_e2e * 1e-3)}
         if graph is not None:
-            ms_main, ms_main_e2e, launches = ms_graph, ms_graph_e2e, \
-                graph.launches_per_step * args.steps
+            ms_main, ms_main_e2e, launches = ms_graph, ms_graph_e2e, launches_graph * args.steps
         else:
             ms_main, ms_main_e2e = ms, ms_e2e
         line = {
