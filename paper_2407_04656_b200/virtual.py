@@ -1,0 +1,91 @@
+"""N virtual EP ranks on ONE GPU, exchanging through device memory (SURVEY.md 4.4
+"single-GPU multi-rank loopback"; BASELINE config 1: "4 simulated EP ranks").
+
+Every virtual rank owns its token batch and its plan column exactly like a real rank;
+the all-gather of the histograms is a device-side stack, and the dispatch / combine use
+the same fused P2P kernels as the multi-GPU path (``lz_pack_p2p`` / ``lz_combine_p2p``)
+with the per-rank receive buffers as the "peers" -- so the N-rank layouts, destination
+rows and kernels are exercised at any N (e.g. 8) on a single device.  Forward only
+(config 1 is a forward benchmark); each virtual rank's experts run through the same
+grouped tcgen05 GEMM.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib, ops
+from .dispatch import plan_device
+from .layer import init_expert
+
+
+class VirtualEP:
+    def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int, replicas,
+                 tokens_per_rank: int, *, seed: int = 0, init_std: float = 0.02,
+                 router_bias=None, router_std: float | None = None, device=None,
+                 activation: str = "gelu"):
+        self.d, self.d_ff, self.E, self.k = d_model, d_ff, n_experts, top_k
+        self.R = [list(r) for r in replicas]
+        self.N = len(self.R[0])
+        self.Tn = tokens_per_rank
+        self.activation = activation
+        dev = torch.device(device) if device is not None else torch.device("cuda")
+        self.device = dev
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        self.wg = (torch.randn(n_experts, d_model, generator=g, device=dev) *
+                   (init_std if router_std is None else router_std)).bfloat16()
+        self.bg = (torch.zeros(n_experts, device=dev) if router_bias is None
+                   else torch.as_tensor(router_bias, dtype=torch.float32, device=dev).clone())
+        self.R_dev = torch.tensor(self.R, dtype=torch.int32, device=dev)
+        # per virtual rank: hosted experts and their weight copies (one per (e, rank))
+        self.local = [[e for e in range(self.E) if self.R[e][r] > 0] for r in range(self.N)]
+        self.w1, self.w2, self.off_index = [], [], []
+        for r in range(self.N):
+            pairs = [init_expert(seed, e, d_model, d_ff, init_std, dev, activation)
+                     for e in self.local[r]]
+            self.w1.append(torch.stack([a for a, _ in pairs]).contiguous() if pairs else None)
+            self.w2.append(torch.stack([b for _, b in pairs]).contiguous() if pairs else None)
+            self.off_index.append(torch.tensor(self.local[r] + [self.E], dtype=torch.long,
+                                               device=dev))
+        align = 256
+        self.cap = (self.N * tokens_per_rank * top_k + self.E * (align - 1) + align - 1) // align * align
+        self.X = torch.empty((self.N, self.cap, d_model), dtype=torch.bfloat16, device=dev)
+        self.Y = torch.empty_like(self.X)
+        self.peers_x = torch.tensor([self.X[r].data_ptr() for r in range(self.N)],
+                                    dtype=torch.int64, device=dev)
+        self.peers_y = torch.tensor([self.Y[r].data_ptr() for r in range(self.N)],
+                                    dtype=torch.int64, device=dev)
+        self.last_plans = None
+
+    @torch.no_grad()
+    def forward(self, xs):
+        """xs: list of N [tokens_per_rank, d] bf16 tensors -> list of N outputs."""
+        N, E, k, d, d_ff = self.N, self.E, self.k, self.d, self.d_ff
+        gates = [ops.router_gate(x, self.wg, self.bg, k) for x in xs]
+        T = torch.stack([gt[3] for gt in gates], dim=1).contiguous()   # all-gather analog
+        align = ops.row_align()
+        plans = [plan_device(T, self.R_dev, r, gates[r][0].view(-1), align) for r in range(N)]
+        self.last_plans = plans
+        for r in range(N):   # every rank scatters its rows into the owners' buffers
+            ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, self.peers_x,
+                         self.X[r], plans[r].recv_m, plans[r].recv_off)
+        swi = self.activation == "swiglu"
+        for r in range(N):
+            if self.w1[r] is None:
+                continue
+            off = plans[r].recv_off.index_select(0, self.off_index[r]).contiguous()
+            H = torch.empty((self.cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16,
+                            device=self.device)
+            A = torch.empty((self.cap, d_ff), dtype=torch.bfloat16, device=self.device)
+            ops.grouped_gemm_rows(self.X[r], self.w1[r], off, A, aux=H,
+                                  epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
+            ops.grouped_gemm_rows(A, self.w2[r], off, self.Y[r])
+        return [ops.combine_p2p(self.peers_y, plans[r].dest_rank, plans[r].dest_row,
+                                gates[r][1], k, d) for r in range(N)]
+
+    __call__ = forward
+
+    def check(self) -> None:
+        for p in self.last_plans or []:
+            p.check()
