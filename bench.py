@@ -98,6 +98,14 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        if not self.lines:   # timed region shorter than the first sample: query once now
+            try:
+                self.lines = subprocess.run(
+                    ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                     "-i", str(self.gpu)], capture_output=True, text=True,
+                    timeout=10).stdout.strip().splitlines()
+            except Exception:
+                pass
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
@@ -476,28 +484,43 @@ def run_virtual(args, cfg):
     for _ in range(max(3, args.warmup)):
         vep(xs)
     torch.cuda.synchronize()
+
+    def eager():
+        outs = vep(xs)
+        return torch.stack([o[0, 0].float() for o in outs]).sum().view(1)
+
+    run, mode = eager, "eager"
     n0 = _lib.launch_count
+    eager()
+    torch.cuda.synchronize()
+    launches = _lib.launch_count - n0
+    if not args.no_graph:
+        # the launch-bound 4K-token forward replays as one CUDA graph (static inputs xs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            gsum = eager()
+        run, mode = (lambda: (graph.replay(), gsum)[1]), "cuda-graph replay"
+        for _ in range(3):
+            run()
+        torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     clk = ClockSampler(local).start()
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record()
-        vep(xs)
+        run()
         ev[i][1].record()
     torch.cuda.synchronize()
-    launches = (_lib.launch_count - n0) // args.steps
     ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
-    # e2e: pinned host tokens -> device, forward, one scalar back per step
-    dx = [torch.empty_like(x) for x in xs]
+    # e2e: pinned host tokens -> the (static) device inputs, forward, one scalar back per step
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
     for i in range(args.steps):
-        for h, t in zip(host, dx):
+        for h, t in zip(host, xs):
             t.copy_(h, non_blocking=True)
-        outs = vep(dx)
-        s = sum(o[0, 0].float() for o in outs).cpu()
+        run().cpu()
     e1.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
@@ -520,7 +543,7 @@ def run_virtual(args, cfg):
             "data": "synthetic (random-init weights, Zipf-biased router)",
             "config": {"workload": cfg["name"], "virtual_ranks": nv, "tokens_per_rank": Tn,
                        "experts": E, "top_k": k, "d_model": d, "d_ff": dff,
-                       "l2": "flushed between timed steps (256 MB write)"},
+                       "l2": "flushed between timed steps (256 MB write)", "mode": mode},
             "roofline": {"kernel": "whole forward step (launch-bound at this size)",
                          "bound": "tensor", "achieved": flops / (ms * 1e-3) / 1e12,
                          "peak": peak_burst, "unit": "TFLOP/s",

@@ -6,8 +6,9 @@ the all-gather of the histograms is a device-side stack, and the dispatch / comb
 the same fused P2P kernels as the multi-GPU path (``lz_pack_p2p`` / ``lz_combine_p2p``)
 with the per-rank receive buffers as the "peers" -- so the N-rank layouts, destination
 rows and kernels are exercised at any N (e.g. 8) on a single device.  Forward only
-(config 1 is a forward benchmark); each virtual rank's experts run through the same
-grouped tcgen05 GEMM.
+(config 1 is a forward benchmark); the experts of ALL virtual ranks run through one
+grouped tcgen05 GEMM launch per layer GEMM (the ranks' receive regions are laid out back
+to back in one buffer).
 """
 
 from __future__ import annotations
@@ -38,51 +39,59 @@ class VirtualEP:
         self.bg = (torch.zeros(n_experts, device=dev) if router_bias is None
                    else torch.as_tensor(router_bias, dtype=torch.float32, device=dev).clone())
         self.R_dev = torch.tensor(self.R, dtype=torch.int32, device=dev)
-        # per virtual rank: hosted experts and their weight copies (one per (e, rank))
+        # hosted experts per virtual rank, one weight copy per (expert, rank) -- all ranks'
+        # copies concatenated so ONE grouped GEMM launch serves every virtual rank
         self.local = [[e for e in range(self.E) if self.R[e][r] > 0] for r in range(self.N)]
-        self.w1, self.w2, self.off_index = [], [], []
+        w1, w2, flat = [], [], []
         for r in range(self.N):
-            pairs = [init_expert(seed, e, d_model, d_ff, init_std, dev, activation)
-                     for e in self.local[r]]
-            self.w1.append(torch.stack([a for a, _ in pairs]).contiguous() if pairs else None)
-            self.w2.append(torch.stack([b for _, b in pairs]).contiguous() if pairs else None)
-            self.off_index.append(torch.tensor(self.local[r] + [self.E], dtype=torch.long,
-                                               device=dev))
+            for e in self.local[r]:
+                a, b = init_expert(seed, e, d_model, d_ff, init_std, dev, activation)
+                w1.append(a)
+                w2.append(b)
+                flat.append(r * (self.E + 1) + e)
+        flat.append((self.N - 1) * (self.E + 1) + self.E)
+        self.w1 = torch.stack(w1).contiguous()
+        self.w2 = torch.stack(w2).contiguous()
+        self.flat = torch.tensor(flat, dtype=torch.long, device=dev)
+        # every rank's receive region is packed right after the previous rank's (bases
+        # computed on the device from the plans), so the concatenated group offsets are
+        # monotonic with no gap rows between ranks
         align = 256
-        self.cap = (self.N * tokens_per_rank * top_k + self.E * (align - 1) + align - 1) // align * align
-        self.X = torch.empty((self.N, self.cap, d_model), dtype=torch.bfloat16, device=dev)
+        self.cap = (self.N * tokens_per_rank * top_k + self.N * self.E * (align - 1) + align - 1
+                    ) // align * align
+        self.X = torch.empty((self.cap, d_model), dtype=torch.bfloat16, device=dev)
         self.Y = torch.empty_like(self.X)
-        self.peers_x = torch.tensor([self.X[r].data_ptr() for r in range(self.N)],
-                                    dtype=torch.int64, device=dev)
-        self.peers_y = torch.tensor([self.Y[r].data_ptr() for r in range(self.N)],
-                                    dtype=torch.int64, device=dev)
+        self._none = torch.empty(0, dtype=torch.int32, device=dev)
         self.last_plans = None
 
     @torch.no_grad()
     def forward(self, xs):
         """xs: list of N [tokens_per_rank, d] bf16 tensors -> list of N outputs."""
         N, E, k, d, d_ff = self.N, self.E, self.k, self.d, self.d_ff
-        gates = [ops.router_gate(x, self.wg, self.bg, k) for x in xs]
+        gates = [ops.router_gate(x, self.wg, self.bg, k, probs=False) for x in xs]
         T = torch.stack([gt[3] for gt in gates], dim=1).contiguous()   # all-gather analog
         align = ops.row_align()
         plans = [plan_device(T, self.R_dev, r, gates[r][0].view(-1), align) for r in range(N)]
         self.last_plans = plans
-        for r in range(N):   # every rank scatters its rows into the owners' buffers
-            ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, self.peers_x,
-                         self.X[r], plans[r].recv_m, plans[r].recv_off)
+        offs = torch.stack([p.recv_off for p in plans]).to(torch.int64)          # [N, E+1]
+        base = torch.cumsum(offs[:, E], 0) - offs[:, E]                         # [N]
+        row_b = 2 * d
+        peers_x = base * row_b + self.X.data_ptr()
+        peers_y = base * row_b + self.Y.data_ptr()
+        off = (offs + base[:, None]).view(-1).index_select(0, self.flat).to(torch.int32)
+        for r in range(N):   # every rank scatters its rows into the owners' regions
+            # forward only: pad rows are never read back, so they are not zeroed (E = 0)
+            ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
+                         self._none, self._none)
         swi = self.activation == "swiglu"
-        for r in range(N):
-            if self.w1[r] is None:
-                continue
-            off = plans[r].recv_off.index_select(0, self.off_index[r]).contiguous()
-            H = torch.empty((self.cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16,
-                            device=self.device)
-            A = torch.empty((self.cap, d_ff), dtype=torch.bfloat16, device=self.device)
-            ops.grouped_gemm_rows(self.X[r], self.w1[r], off, A, aux=H,
-                                  epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
-            ops.grouped_gemm_rows(A, self.w2[r], off, self.Y[r])
-        return [ops.combine_p2p(self.peers_y, plans[r].dest_rank, plans[r].dest_row,
-                                gates[r][1], k, d) for r in range(N)]
+        H = torch.empty((self.cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16,
+                        device=self.device)
+        A = torch.empty((self.cap, d_ff), dtype=torch.bfloat16, device=self.device)
+        ops.grouped_gemm_rows(self.X, self.w1, off, A, aux=H,
+                              epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
+        ops.grouped_gemm_rows(A, self.w2, off, self.Y)
+        return [ops.combine_p2p(peers_y, plans[r].dest_rank, plans[r].dest_row, gates[r][1],
+                                k, d) for r in range(N)]
 
     __call__ = forward
 
