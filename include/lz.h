@@ -99,6 +99,13 @@ lz_status lz_shuffle_index(const int32_t* send_counts, int E, int N, const int32
                            int32_t* slot, int32_t* gather, int32_t* err, void* ws,
                            size_t ws_bytes, void* stream);
 
+/* Routing-history window: ring[(pos % W) * E + e] = sum_j T[e*N + j]; ++pos (device).
+ * Replaces the reference's per-step load snapshot appended to the trailing window
+ * (simulator.py:642-644); window_loads (simulator.py:342-351) = sum of the first
+ * min(pos, W) ring rows // min(pos, W), computed by the host at a rebalance. */
+lz_status lz_load_record(const int32_t* T, int E, int N, int64_t* ring, int W, int64_t* pos,
+                         void* stream);
+
 /* ------------------------------------------------------------------- K1 gating */
 
 /* softmax over E logits, top-k (ties -> lower expert id), weights = top-k probs

@@ -472,3 +472,29 @@ extern "C" lz_status lz_shuffle_index(const int32_t* send_counts, int E, int N,
   }
   return LZ_OK;
 }
+
+// Routing-history accumulator: one step's global per-expert load
+// (row sums of the all-gathered T) into slot pos % W of a device ring, pos advanced on
+// the device -- so the record is CUDA-graph safe.  The host reads the window only at a
+// rebalance (simulator.py:342-351 window_loads; :642-644 trailing window of W steps).
+__global__ void load_record_kernel(const int32_t* __restrict__ T, int E, int N,
+                                   int64_t* __restrict__ ring, int W, int64_t* __restrict__ pos) {
+  const int64_t p = *pos;
+  const int64_t slot = p % W;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int64_t s = 0;
+    for (int j = 0; j < N; ++j) s += T[(size_t)e * N + j];
+    ring[slot * E + e] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *pos = p + 1;
+}
+
+extern "C" lz_status lz_load_record(const int32_t* T, int E, int N, int64_t* ring, int W,
+                                    int64_t* pos, void* stream) {
+  lz_status st = check_EN(E, N);
+  if (st != LZ_OK) return st;
+  if (!T || !ring || !pos || W < 1) return LZ_ERR_ARG;
+  load_record_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(T, E, N, ring, W, pos);
+  return lzh::check_launch();
+}

@@ -24,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from .placement import (ClusterSpec, allocate_replicas, build_mro_plan, greedy_node_mapping,
-                        node_order, replica_matrix)
+                        node_order, plan_state_transfers, replica_matrix)
 
 
 def replan(loads: Sequence[int], live_nodes: Sequence[int], holdings: dict, slots: int,
@@ -45,24 +45,40 @@ def transfer_schedule(new_R, new_nodes: Sequence[int], holdings: dict):
     is the surviving owner with the fewest sends of that expert, then fewest sends
     overall, then the lowest node id (plan_state_transfers, migration.py:164-195).
     Experts with no surviving owner are returned separately (checkpoint fallback)."""
-    per_item: dict = {}
-    total: dict = {}
-    out, orphans = [], []
-    work = []
-    for r, node in enumerate(new_nodes):
-        for e, row in enumerate(new_R):
-            if row[r] > 0 and e not in holdings.get(node, set()):
-                work.append((e, node))
-    for e, node in sorted(work, key=lambda w: (repr(w[0]), w[1])):
-        owners = [v for v in sorted(holdings) if e in holdings[v] and v != node]
-        if not owners:
-            orphans.append((e, node))
-            continue
-        src = min(owners, key=lambda o: (per_item.get((e, o), 0), total.get(o, 0), o))
-        per_item[(e, src)] = per_item.get((e, src), 0) + 1
-        total[src] = total.get(src, 0) + 1
-        out.append((e, src, node))
-    return out, orphans
+    fetch = {node: {e for e, row in enumerate(new_R) if row[r] > 0} - holdings.get(node, set())
+             for r, node in enumerate(new_nodes)}
+    owners: dict = {}
+    for v in sorted(holdings):
+        for e in holdings[v]:
+            owners.setdefault(e, []).append(v)
+    return plan_state_transfers(fetch, owners, allow_orphans=True)
+
+
+def exchange_expert_state(layers, transfers, me: int, rank_of: dict, group) -> list[dict]:
+    """Batched NCCL send/recv (one ``batch_isend_irecv``) of the expert weights in
+    ``transfers`` = [((layer index, expert), src_node, dst_node)].  Returns, per layer,
+    {expert: (w1, w2)} = this rank's kept experts plus the received ones."""
+    keep = [layer.expert_state() for layer in layers]
+    got: list[dict] = [dict(k) for k in keep]
+    ops = []
+    for (li, e), src, dst in transfers:
+        layer = layers[li]
+        if src == me:
+            w1, w2 = keep[li][e]
+            ops.append(dist.P2POp(dist.isend, w1.contiguous(), rank_of[dst], group))
+            ops.append(dist.P2POp(dist.isend, w2.contiguous(), rank_of[dst], group))
+        elif dst == me:
+            f1 = 2 * layer.d_ff if layer.activation == "swiglu" else layer.d_ff
+            b1 = torch.empty((f1, layer.d), dtype=torch.bfloat16, device=layer.device)
+            b2 = torch.empty((layer.d, layer.d_ff), dtype=torch.bfloat16, device=layer.device)
+            ops.append(dist.P2POp(dist.irecv, b1, rank_of[src], group))
+            ops.append(dist.P2POp(dist.irecv, b2, rank_of[src], group))
+            got[li][e] = (b1, b2)
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    torch.cuda.synchronize()
+    return got
 
 
 def shrink_and_replan(layer, group, exclude: Sequence[int], loads: Sequence[int], slots: int,
@@ -82,29 +98,9 @@ def shrink_and_replan(layer, group, exclude: Sequence[int], loads: Sequence[int]
     new_nodes = live  # communicator rank r <-> node live[r]
     me = nodes[old_rank]
     transfers, orphans = transfer_schedule(R, new_nodes, holdings)
-    # keep local copies, then exchange the weights of newly hosted experts
-    keep = layer.expert_state()
-    recv: dict = {}
-    ops = []
     rank_of = {v: r for r, v in enumerate(new_nodes)}
-    for e, src, dst in transfers:
-        if src == me:
-            w1, w2 = keep[e]
-            ops.append(dist.P2POp(dist.isend, w1.contiguous(), rank_of[dst], new_group))
-            ops.append(dist.P2POp(dist.isend, w2.contiguous(), rank_of[dst], new_group))
-        elif dst == me:
-            f1 = 2 * layer.d_ff if layer.activation == "swiglu" else layer.d_ff
-            b1 = torch.empty((f1, layer.d), dtype=torch.bfloat16, device=layer.device)
-            b2 = torch.empty((layer.d, layer.d_ff), dtype=torch.bfloat16, device=layer.device)
-            ops.append(dist.P2POp(dist.irecv, b1, rank_of[src], new_group))
-            ops.append(dist.P2POp(dist.irecv, b2, rank_of[src], new_group))
-            recv[e] = (b1, b2)
-    if ops:
-        for req in dist.batch_isend_irecv(ops):
-            req.wait()
-    torch.cuda.synchronize()
-    weights = dict(keep)
-    weights.update(recv)
+    weights = exchange_expert_state([layer], [((0, e), src, dst) for e, src, dst in transfers],
+                                    me, rank_of, new_group)[0]
     layer.group = new_group
     layer.rank = dist.get_rank(new_group)
     layer.world = dist.get_world_size(new_group)

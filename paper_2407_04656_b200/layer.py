@@ -104,6 +104,7 @@ class MoELayer(torch.nn.Module):
         self._symm_group = None
         self._fwd_version = 0
         self.stage_events: list | None = None
+        self.load_window = None   # rebalance.LoadWindow, attached by rebalance.Rebalancer
         # SMs the backward GEMMs leave to NCCL while the expert-gradient all-reduce runs
         self.overlap_reserve = int(os.environ.get("LZ_OVERLAP_SMS", "16"))
         self.set_plan(replicas)
@@ -229,6 +230,8 @@ class _MoEFunction(torch.autograd.Function):
         idx, w, probs, hist = ops.router_gate(x, wg, bg, k, layer.renorm)
         _mark(layer, "gate")
         T = comm.allgather_hist(hist, group)
+        if layer.load_window is not None:   # routing history for the periodic rebalance
+            layer.load_window.record(T)
         _mark(layer, "hist_allgather")
         plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ops.row_align())
         layer.last_plan = plan

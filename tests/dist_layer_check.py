@@ -1,6 +1,6 @@
 """Multi-rank MoE layer check (run under torchrun, one rank per GPU, NCCL):
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_layer_check.py [--elastic]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 tests/dist_layer_check.py [--elastic] [--rebalance]
 
 Every rank routes its own tokens through the flexible all-to-all; outputs, input
 grads and the replica-group-summed expert grads are compared with the torch-CPU
@@ -94,6 +94,23 @@ def main():
                      router_bias=bias)
     check(layer, dist.group.WORLD, Tn, 100, f"N={n}")
     group = dist.group.WORLD
+    if "--rebalance" in sys.argv:
+        # the routing skew moves (new hot experts): the device load window sees it and the
+        # periodic rebalance re-places replicas, migrating expert weights over NVLink
+        from paper_2407_04656_b200.rebalance import Rebalancer
+        rb = Rebalancer([layer], c, 2, interval=3)
+        layer.bg.data.copy_(zipf_router_bias(E, 2.0, seed=11).to(layer.bg.device))
+        g = torch.Generator(device="cuda")
+        g.manual_seed(rank)
+        rep = None
+        with torch.no_grad():
+            for _ in range(3):
+                layer(torch.randn(Tn, d, generator=g, device="cuda").bfloat16())
+                rep = rb.step() or rep
+        assert rep is not None and rep["changed"], rep
+        if rank == 0:
+            print(f"rebalance: {rep}", flush=True)
+        check(layer, group, Tn, 300, f"N={n} after rebalance")
     if elastic and n > 2:
         from paper_2407_04656_b200.elastic import shrink_and_replan
         # 8 -> 6 -> 4 when launched on 8 GPUs (4 -> 3 -> 2 on 4): drop two ranks, twice

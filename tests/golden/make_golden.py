@@ -63,7 +63,7 @@ def main() -> None:
     from flexep.dispatch import (ReplicaMatrix, UnroutableTokenError, build_shuffle_index,
                                  compute_dispatch_schedule, full_dispatch_matrices,
                                  simulate_all_to_all)
-    from flexep.migration import greedy_node_mapping
+    from flexep.migration import greedy_node_mapping, plan_state_transfers
     from flexep.placement import build_mro_plan
 
     out: dict = {"generator": "tests/golden/make_golden.py", "reference": "flexep 0.1.0"}
@@ -216,6 +216,45 @@ def main() -> None:
                      "live": live, "new_slots": [list(x) for x in new.slots],
                      "assignment": [list(a) for a in m.assignment]})
     pl["node_mapping"] = maps
+    # periodic rebalance over L layers (rebuild_adaptive_plans, simulator.py:363-384):
+    # joint (layer, expert) greedy mapping + plan_state_transfers (migration.py:164-195)
+    reb = []
+    rng = random.Random(0x2EBA)
+    for _ in range(60):
+        L = rng.choice([1, 2, 4])
+        E = rng.choice([8, 16, 32])
+        n = rng.choice([2, 3, 4, 6, 8])
+        c = rng.choice([-(-3 * E // n), -(-5 * E // n)])
+        f = min(2, n)
+        spec = ClusterSpec(n_nodes=n, slots_per_node=c, fault_threshold=f)
+        old_loads, new_loads, old_slots = [], [], []
+        for li in range(L):
+            s0, s1 = rng.choice([0.0, 1.2, 2.5]), rng.choice([0.0, 1.2, 2.5])
+            p0, p1 = list(range(E)), list(range(E))
+            rng.shuffle(p0)
+            rng.shuffle(p1)
+            old_loads.append([int(1e4 * (1 + p0[e]) ** (-s0)) + 1 for e in range(E)])
+            new_loads.append([int(1e4 * (1 + p1[e]) ** (-s1)) + 1 for e in range(E)])
+        old = [build_mro_plan(allocate_replicas(old_loads[li], spec), spec, layer=li)
+               for li in range(L)]
+        live = list(range(n))
+        held = {v: {(li, ex) for li in range(L) for ex in old[li].col_sets[v]} for v in live}
+        new = [build_mro_plan(allocate_replicas(new_loads[li], spec), spec, layer=li)
+               for li in range(L)]
+        cols = [{(li, ex) for li in range(L) for ex in new[li].col_sets[j]} for j in range(n)]
+        m = greedy_node_mapping(held, cols, live)
+        owners = {}
+        for v in live:
+            for item in held[v]:
+                owners.setdefault(item, []).append(v)
+        sched = plan_state_transfers(m, owners)
+        reb.append({"n": n, "c": c, "f": f, "E": E,
+                    "old_R": [[list(x) for x in ReplicaMatrix.from_plan(p).counts] for p in old],
+                    "loads": new_loads,
+                    "new_slots": [[list(x) for x in p.slots] for p in new],
+                    "assignment": [list(a) for a in m.assignment],
+                    "transfers": [[list(t.item), t.source, t.dest] for t in sched.transfers]})
+    pl["rebalance"] = reb
     with open(os.path.join(HERE, "placement_golden.json"), "w") as f:
         json.dump(pl, f, separators=(",", ":"))
     print("wrote golden vectors")
