@@ -8,7 +8,7 @@ import os
 import threading
 
 _DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_DIR, "liblz.so")
+LIB_PATH = os.environ.get("LZ_LIB_PATH") or os.path.join(_DIR, "liblz.so")  # override: A/B builds (tools/)
 
 _vp, _i, _sz, _fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p
 

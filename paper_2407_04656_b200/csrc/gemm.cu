@@ -118,14 +118,22 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// arrive on the barrier at the same smem offset in CTA `cta` of the cluster
+// arrive on the barrier at the same smem offset in CTA `cta` of the cluster.  Relaxed:
+// it only signals "TMEM accumulator drained" -- the tcgen05.ld data is already in
+// registers (tcgen05.wait::ld), so no memory needs releasing, and a release.cluster
+// arrive costs MEMBAR.ALL.GPU + ERRBAR per epilogue warp per tile (ncu r01c).
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\t"
       "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
       "r"(cta)
       : "memory");
+}
+// the accumulator-empty barrier lives in the leader CTA (rank 0), which issues the MMAs
+__device__ __forceinline__ void tmem_release(uint64_t* bar, int cg) {
+  if (cg == 1 || cluster_ctarank() == 0) mbar_arrive(bar);
+  else mbar_arrive_cluster(bar, 0);
 }
 template <int CG>
 __device__ __forceinline__ void tc_commit_cg(uint64_t* bar) {
@@ -264,6 +272,42 @@ __device__ __forceinline__ void gelu_and_grad(float x, float& y, float& dy) {
   y = 0.5f * x * (1.f + t);
   dy = 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * kS2PI * fmaf(3.f * kGC, x2, 1.f);
 }
+// Packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2): half the issue slots of scalar FP32
+// for the epilogue math, which is issue/latency-bound next to the tensor pipe.
+__device__ __forceinline__ unsigned long long f2_u64(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 u64_f2(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0,%1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)), "l"(f2_u64(c)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_u64(a)), "l"(f2_u64(b)));
+  return u64_f2(r);
+}
+__device__ __forceinline__ float2 splat2(float v) { return make_float2(v, v); }
+// gelu and gelu' of two values, 10 packed ops + 2 tanh:  s = (1 + t) / 2,  gelu = x s,
+// gelu' = s + x (-2 q) s (s - 1)  with  q = du/dx = c0 (1 + 3 kGC x^2)  (1 - t^2 = 4 s (1 - s))
+__device__ __forceinline__ void gelu_and_grad2(float2 x, float2& y, float2& dy) {
+  constexpr float c0 = kS2PI, c1 = kS2PI * kGC;
+  const float2 x2 = mul2(x, x);
+  const float2 u = mul2(x, fma2(x2, splat2(c1), splat2(c0)));
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 sv = fma2(t, splat2(0.5f), splat2(0.5f));
+  const float2 z = fma2(t, splat2(0.5f), splat2(-0.5f));
+  const float2 wn = mul2(x, fma2(x2, splat2(-6.f * c1), splat2(-2.f * c0)));
+  y = mul2(x, sv);
+  dy = fma2(wn, mul2(sv, z), sv);
+}
 __device__ __forceinline__ float gelu_f(float x) {
   const float u = kS2PI * fmaf(kGC * x, x * x, x);
   return 0.5f * x * (1.f + tanh_fast(u));
@@ -395,10 +439,7 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
     if (c == nchunks - 1) {
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        if (cg == 1) mbar_arrive(tempty);
-        else mbar_arrive_cluster(tempty, 0);
-      }
+      if (lane == 0) tmem_release(tempty, cg);
     }
     float g[32], u[32];
     if (fwd) {
@@ -679,10 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           // accumulator fully read: hand TMEM back to the MMA issuer early
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) {
-            if (CG == 1) mbar_arrive(&tempty_bar[acc]);
-            else mbar_arrive_cluster(&tempty_bar[acc], 0);
-          }
+          if (lane == 0) tmem_release(&tempty_bar[acc], CG);
         }
         float f[32];
 #pragma unroll
@@ -696,7 +734,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             float h[8];
             bf16x8_to_f32(ld_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q)), h);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) f[8 * q + i] *= h[i];
+            for (int i = 0; i < 8; i += 2) {
+              const float2 m = mul2(make_float2(f[8 * q + i], f[8 * q + i + 1]),
+                                    make_float2(h[i], h[i + 1]));
+              f[8 * q + i] = m.x;
+              f[8 * q + i + 1] = m.y;
+            }
           }
         }
         // the store that used buffer b (chunk c-2) must have finished reading smem
@@ -711,7 +754,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (gelu) {
           float dg[32];
 #pragma unroll
-          for (int q = 0; q < 32; ++q) gelu_and_grad(f[q], f[q], dg[q]);
+          for (int q = 0; q < 32; q += 2) {
+            float2 y2, d2;
+            gelu_and_grad2(make_float2(f[q], f[q + 1]), y2, d2);
+            f[q] = y2.x;
+            f[q + 1] = y2.y;
+            dg[q] = d2.x;
+            dg[q + 1] = d2.y;
+          }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(dg + 8 * q));
