@@ -263,15 +263,8 @@ __device__ __forceinline__ float tanh_fast(float x) {
 }
 constexpr float kS2PI = 0.7978845608028654f;
 constexpr float kGC = 0.044715f;
-// GELU and its derivative from one tanh: the forward epilogue stores gelu'(h) (not h) as
-// the backward's aux stream, so the dGELU epilogue is a plain multiply (no MUFU in the
-// backward GEMM epilogue)
-__device__ __forceinline__ void gelu_and_grad(float x, float& y, float& dy) {
-  const float x2 = x * x;
-  const float t = tanh_fast(kS2PI * fmaf(kGC * x, x2, x));
-  y = 0.5f * x * (1.f + t);
-  dy = 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * kS2PI * fmaf(3.f * kGC, x2, 1.f);
-}
+// The forward GELU epilogue stores gelu'(h) (not h) as the backward's aux stream, so the
+// dGELU epilogue is a plain multiply (no MUFU in the backward GEMM epilogue).
 // Packed fp32x2 arithmetic (sm_100 FFMA2 / FMUL2): half the issue slots of scalar FP32
 // for the epilogue math, which is issue/latency-bound next to the tensor pipe.
 __device__ __forceinline__ unsigned long long f2_u64(float2 v) {
@@ -307,15 +300,6 @@ __device__ __forceinline__ void gelu_and_grad2(float2 x, float2& y, float2& dy) 
   const float2 wn = mul2(x, fma2(x2, splat2(-6.f * c1), splat2(-2.f * c0)));
   y = mul2(x, sv);
   dy = fma2(wn, mul2(sv, z), sv);
-}
-__device__ __forceinline__ float gelu_f(float x) {
-  const float u = kS2PI * fmaf(kGC * x, x * x, x);
-  return 0.5f * x * (1.f + tanh_fast(u));
-}
-__device__ __forceinline__ float dgelu_f(float x) {
-  const float x2 = x * x;
-  const float t = tanh_fast(kS2PI * fmaf(kGC * x, x2, x));
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * kS2PI * fmaf(3.f * kGC, x2, 1.f);
 }
 
 struct Params {
@@ -389,7 +373,6 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
 //            interleaved H[rows, 2N] and writes dH = [dG | dU] into C[rows, 2N]
 // Each epilogue warp owns 32 rows and one half of the tile's hidden units; single-
 // buffered staging (4 x 2 KB per warp), next chunk's G/U loads overlap the current chunk.
-__device__ __forceinline__ float sigmoid_f(float x) { return 0.5f * (1.f + tanh_fast(0.5f * x)); }
 
 __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const TileInfo& t,
                                              int row0, int half, int lane, uint32_t tbase,
@@ -472,12 +455,22 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
       //   S = silu(g) (gate column), Q = u * silu'(g) (up column); act = S * u
       float a[32];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const float sg = sigmoid_f(g[q]);
-        const float sl = g[q] * sg;
-        a[q] = sl * u[q];
-        u[q] = u[q] * sg * (1.f + g[q] * (1.f - sg));
-        g[q] = sl;
+      for (int q = 0; q < 32; q += 2) {
+        // packed: sg = (1 + tanh(g/2)) / 2, S = g sg, act = S u, Q = u sg (1 + g (1 - sg))
+        const float2 g2 = make_float2(g[q], g[q + 1]), u2 = make_float2(u[q], u[q + 1]);
+        const float2 h2 = mul2(g2, splat2(0.5f));
+        const float2 t2 = make_float2(tanh_fast(h2.x), tanh_fast(h2.y));
+        const float2 sg = fma2(t2, splat2(0.5f), splat2(0.5f));
+        const float2 om = fma2(t2, splat2(-0.5f), splat2(0.5f));
+        const float2 sl = mul2(g2, sg);
+        const float2 a2 = mul2(sl, u2);
+        const float2 q2 = mul2(mul2(u2, sg), fma2(g2, om, splat2(1.f)));
+        a[q] = a2.x;
+        a[q + 1] = a2.y;
+        u[q] = q2.x;
+        u[q + 1] = q2.y;
+        g[q] = sl.x;
+        g[q + 1] = sl.y;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -496,10 +489,15 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
     } else {
       float dg[32], du[32];
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const float da = __uint_as_float(va[q]);  // g holds S = silu(g), u holds Q
-        du[q] = da * g[q];
-        dg[q] = da * u[q];
+      for (int q = 0; q < 32; q += 2) {
+        // g holds S = silu(g), u holds Q
+        const float2 da = make_float2(__uint_as_float(va[q]), __uint_as_float(va[q + 1]));
+        const float2 a = mul2(da, make_float2(g[q], g[q + 1]));
+        const float2 b = mul2(da, make_float2(u[q], u[q + 1]));
+        du[q] = a.x;
+        du[q + 1] = a.y;
+        dg[q] = b.x;
+        dg[q + 1] = b.y;
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {

@@ -50,9 +50,9 @@ def main():
         "dgrad1": lambda: ops.grouped_gemm_rows(dA, W1, off, dX, b_major=_lib.LZ_MN_MAJOR),
     }
     n_mat = 3 if a.swiglu else 2
-    flops = {k: 2 * rows * d * dff * (1.5 if a.swiglu and k in ("fwd1+act", "dgrad2+dact", "wgrad1",
-                                                                 "dgrad1") else 1)
-             for k in ops_}
+    # fwd1 / wgrad1 / dgrad1 touch W1 (2 d_ff rows for SwiGLU: gate | up)
+    flops = {k: 2 * rows * d * dff * (2 if a.swiglu and k in ("fwd1+act", "wgrad1", "dgrad1")
+                                      else 1) for k in ops_}
     tot = 0.0
     for name, fn in ops_.items():
         for _ in range(3):
