@@ -29,22 +29,25 @@ constexpr int kMaxGroups = 128;
 // (GELU pre-activation out / dGELU pre-activation in)
 constexpr int kEpiCols = 32;
 constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
-constexpr int kEpiWarpBytes = 4 * kEpiBuf;          // out0 out1 aux0 aux1
-constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;  // 64 KB
 constexpr int kBarBytes = 256;
-constexpr int kTabBytes = 2 * (kMaxGroups + 1) * 4;
+constexpr int kTabBytes = 3 * (kMaxGroups + 1) * 4;  // s_off, s_pref, s_perm
 
-// CG = 1: one CTA per 128 x 256 tile (UMMA 128x256x16, cta_group::1), 4 stages x 48 KB.
+// CG = 1: one CTA per 128 x 256 tile (UMMA 128x256x16, cta_group::1), 3-4 stages x 48 KB.
 // CG = 2: a CTA pair per 256 x 256 tile (UMMA 256x256x16, cta_group::2): each CTA stages
-//         its 128 rows of A and half (128 columns) of B -> 32 KB/stage, 6 stages; the
+//         its 128 rows of A and half (128 columns) of B -> 32 KB/stage, 5-6 stages; the
 //         leader CTA issues the MMAs for both, halving per-SM smem operand traffic.
-template <int CG>
+// AUX: the epilogue has an aux stream (GELU/dGELU/SwiGLU/dSwiGLU) -> 8 KB of staging per
+// epilogue warp (out0 out1 aux0 aux1); plain stores need 4 KB, and the freed 32 KB buys
+// one more operand stage (deeper TMA prefetch for the K = 4096 GEMMs).
+template <int CG, bool AUX>
 struct Cfg {
+  static constexpr int kEpiWarpBytes = (AUX ? 4 : 2) * kEpiBuf;
+  static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
   static constexpr int kBRows = BN / CG;                 // B rows (n) staged per CTA
   static constexpr int kATileBytes = BM * BK * 2;        // 16 KB
   static constexpr int kBTileBytes = kBRows * BK * 2;    // 32 KB / 16 KB
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CG == 1 ? 3 : 5;
+  static constexpr int kStages = CG == 1 ? (AUX ? 3 : 4) : (AUX ? 5 : 6);
   static constexpr int kTilesBytes = kStages * kStageBytes;
   static constexpr int kTileM = BM * CG;                 // rows per (pair) tile
   static constexpr int kSmemBytes = 1024 + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
@@ -345,9 +348,10 @@ struct TileInfo {
 
 template <int CG>
 __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
-                                                const int32_t* s_off, int tile) {
-  // (tiles are TileM x BN; mb counts TileM blocks)
-  // binary search the group: s_pref[g] <= tile < s_pref[g+1]
+                                                const int32_t* s_off, const int32_t* s_perm,
+                                                int tile) {
+  // (tiles are TileM x BN; mb counts TileM blocks).  Tiles are numbered over the groups
+  // in s_perm order: binary search the position i with s_pref[i] <= tile < s_pref[i+1]
   int lo = 0, hi = p.G - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -355,13 +359,21 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
     else hi = mid - 1;
   }
   TileInfo t;
-  t.g = lo;
+  t.g = s_perm[lo];
   const int local = tile - s_pref[lo];
   const int nbn = p.N / BN;
   t.mb = local / nbn;
   t.nb = local % nbn;
-  t.nk = (p.mode == 0) ? p.K / BK : (s_off[lo + 1] - s_off[lo]) / BK;
+  t.nk = (p.mode == 0) ? p.K / BK : (s_off[t.g + 1] - s_off[t.g]) / BK;
   return t;
+}
+
+// Static persistent schedule: wave w hands tile w*nunits + slot to unit `unit`, with the
+// slot order reversed on odd waves ("snake").  With tiles numbered in descending cost
+// (weight-gradient groups sorted by their K = rows) this is the LPT-style balance a
+// round-robin over expert-major tiles lacks (ncu r01c: wgrad 80 % vs 88 % tensor-active).
+__device__ __forceinline__ int sched_tile(int w, int unit, int nunits) {
+  return w * nunits + ((w & 1) ? nunits - 1 - unit : unit);
 }
 
 // SwiGLU epilogues (Mixtral experts).  W1|W3 are interleaved in blocks of 128 output
@@ -515,18 +527,18 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
   }
 }
 
-template <int A_MN, int B_MN, int CG>
+template <int A_MN, int B_MN, int CG, bool AUX>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
                         const __grid_constant__ CUtensorMap map_x, const Params p) {
-  using C = Cfg<CG>;
+  using C = Cfg<CG, AUX>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* s_tiles = smem;
   uint8_t* s_epi = smem + C::kTilesBytes;
-  uint64_t* full_bar = (uint64_t*)(s_epi + kEpiBytes);
+  uint64_t* full_bar = (uint64_t*)(s_epi + C::kEpiBytes);
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -541,14 +553,30 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int unit = CG == 1 ? blockIdx.x : (blockIdx.x >> 1);   // tile-processing unit
   const int nunits = CG == 1 ? gridDim.x : (gridDim.x >> 1);
 
-  // group table -> tile prefix (every CTA computes it; G <= kMaxGroups)
+  // group table -> tile prefix (every CTA computes it; G <= kMaxGroups).  Weight-gradient
+  // groups are visited in descending K (tile cost); row GEMM tiles all cost the same.
+  int32_t* s_perm = s_pref + kMaxGroups + 1;
   for (int g = threadIdx.x; g <= p.G; g += blockDim.x) s_off[g] = p.off[g];
+  __syncthreads();
+  for (int g = threadIdx.x; g < p.G; g += blockDim.x) {
+    int rank = g;
+    if (p.mode == 1) {
+      const int kg = s_off[g + 1] - s_off[g];
+      rank = 0;
+      for (int h = 0; h < p.G; ++h) {
+        const int kh = s_off[h + 1] - s_off[h];
+        rank += (kh > kg) || (kh == kg && h < g);
+      }
+    }
+    s_perm[rank] = g;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0;
     const int nbn = p.N / BN;
-    for (int g = 0; g < p.G; ++g) {
-      s_pref[g] = acc;
+    for (int i = 0; i < p.G; ++i) {
+      const int g = s_perm[i];
+      s_pref[i] = acc;
       acc += (p.mode == 0) ? ((s_off[g + 1] - s_off[g]) / C::kTileM) * nbn
                            : (p.M / C::kTileM) * nbn;
     }
@@ -595,8 +623,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ===== TMA producer (both CTAs of a pair load their halves) =====
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < total; tile += nunits) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
+      for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
+           tile = sched_tile(++w, unit, nunits)) {
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
         for (int kb = 0; kb < t.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = s_tiles + stage * C::kStageBytes;
@@ -629,8 +658,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = unit; tile < total; tile += nunits) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
+      for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
+           tile = sched_tile(++w, unit, nunits)) {
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -667,18 +697,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quad = warp & 3;          // TMEM lane quadrant this warp may access
     const int ew = warp - 2;            // epilogue warp index
     const int half = ew >> 2;           // column half of the tile this warp owns
-    uint8_t* wbuf = s_epi + ew * kEpiWarpBytes;
+    uint8_t* wbuf = s_epi + ew * C::kEpiWarpBytes;
     const uint32_t out_s = smem_u32(wbuf);                 // out0, out1
     const uint32_t aux_s = smem_u32(wbuf + 2 * kEpiBuf);   // aux0, aux1
     uint64_t* my_aux_bar = aux_bar + ew * 2;
     uint32_t aux_phase[2] = {0, 0};
-    const bool gelu = p.epilogue == LZ_EPI_GELU, dgelu = p.epilogue == LZ_EPI_DGELU;
-    const bool swiglu = p.epilogue == LZ_EPI_SWIGLU, dswiglu = p.epilogue == LZ_EPI_DSWIGLU;
+    const bool gelu = AUX && p.epilogue == LZ_EPI_GELU, dgelu = AUX && p.epilogue == LZ_EPI_DGELU;
+    const bool swiglu = AUX && p.epilogue == LZ_EPI_SWIGLU;
+    const bool dswiglu = AUX && p.epilogue == LZ_EPI_DSWIGLU;
     constexpr int kChunks = BN / kEpiCols / (kEpiWarps / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = unit; tile < total; tile += nunits) {
-      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, tile);
+    for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
+           tile = sched_tile(++w, unit, nunits)) {
+      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
@@ -850,21 +882,21 @@ extern "C" int lz_gemm_set_cta_group(int cg) {
 }
 extern "C" int lz_gemm_row_align(void) { return BM * g_cta_group; }
 
-template <int A_MN, int B_MN, int CG>
+template <int A_MN, int B_MN, int CG, bool AUX>
 static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, CG>;
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, CG, AUX>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<CG>::kSmemBytes) != cudaSuccess)
+                             Cfg<CG, AUX>::kSmemBytes) != cudaSuccess)
       return lzh::check_launch();
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg<CG>::kSmemBytes;
+  cfg.dynamicSmemBytes = Cfg<CG, AUX>::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -877,18 +909,25 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   return lzh::check_launch();
 }
 
-template <int A_MN, int B_MN>
+template <int A_MN, int B_MN, bool AUX>
 static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                            const CUtensorMap& mx, const Params& p, long tiles, int sms,
                            cudaStream_t s) {
   if (g_cta_group == 2) {
     long units = tiles < sms / 2 ? tiles : sms / 2;
     if (units < 1) units = 1;
-    return launch<A_MN, B_MN, 2>(ma, mb, mc, mx, p, (int)(2 * units), s);
+    return launch<A_MN, B_MN, 2, AUX>(ma, mb, mc, mx, p, (int)(2 * units), s);
   }
   long grid = tiles < sms ? tiles : sms;
   if (grid < 1) grid = 1;
-  return launch<A_MN, B_MN, 1>(ma, mb, mc, mx, p, (int)grid, s);
+  return launch<A_MN, B_MN, 1, AUX>(ma, mb, mc, mx, p, (int)grid, s);
+}
+template <int A_MN, int B_MN>
+static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                           const CUtensorMap& mx, const Params& p, long tiles, int sms,
+                           cudaStream_t s) {
+  return p.epilogue == LZ_EPI_STORE ? launch_cg<A_MN, B_MN, false>(ma, mb, mc, mx, p, tiles, sms, s)
+                                    : launch_cg<A_MN, B_MN, true>(ma, mb, mc, mx, p, tiles, sms, s);
 }
 
 extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
