@@ -194,6 +194,11 @@ lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn, int d, in
 #define LZ_EPI_STORE 0     /* C = acc (bf16)                                   */
 #define LZ_EPI_GELU 1      /* C = gelu(acc), AUX = gelu'(acc) (bf16; the backward factor)   */
 #define LZ_EPI_DGELU 2     /* C = acc * AUX   (AUX as written by LZ_EPI_GELU)             */
+/* Every AUX buffer (GELU/DGELU [rows, N]; SWIGLU/DSWIGLU [S | Q]) has the byte size of a
+ * row-major bf16 [rows, W] matrix but a private 32x32-blocked layout (element (r, c) at
+ * ((r/32)*(W/32) + c/32)*1024 + ((c%32)/8)*256 + (r%32)*8 + c%8) that keeps the
+ * epilogue's accesses coalesced without shared-memory staging; it is produced and
+ * consumed only by the forward / backward epilogue pair. */
 #define LZ_EPI_SWIGLU 3    /* B rows = W1|W3 interleaved in 128-row blocks; with g|u = acc:
                               C[rows, N/2] = silu(g) * u, AUX[rows, N] = [silu(g) | u silu'(g)] */
 #define LZ_EPI_DSWIGLU 4   /* acc = dA[rows, N]; AUX = LZ_EPI_SWIGLU's [S | Q] [rows, 2N];

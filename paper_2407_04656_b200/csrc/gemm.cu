@@ -13,6 +13,8 @@
 // (one weight copy per (expert, rank); R[e][j] > 1 only scales capacity).
 #include <cuda.h>  // CUtensorMap (header only; the encoder is fetched at run time)
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace lz {
@@ -25,8 +27,8 @@ constexpr int kAccCols = BN;              // fp32 accumulator columns per buffer
 constexpr int kTmemCols = 2 * kAccCols;   // 512
 constexpr int kMaxGroups = 128;
 // epilogue staging: each epilogue warp owns 32 rows; chunks of 32 columns (64 B rows,
-// 64B-swizzled, 2 KB) double-buffered for the output and for the aux stream
-// (GELU pre-activation out / dGELU pre-activation in)
+// 64B-swizzled, 2 KB), double-buffered, feed the TMA stores of the outputs (aux streams
+// go straight between registers and global memory, see aux_block)
 constexpr int kEpiCols = 32;
 constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
 constexpr int kBarBytes = 256;
@@ -36,18 +38,19 @@ constexpr int kTabBytes = 3 * (kMaxGroups + 1) * 4;  // s_off, s_pref, s_perm
 // CG = 2: a CTA pair per 256 x 256 tile (UMMA 256x256x16, cta_group::2): each CTA stages
 //         its 128 rows of A and half (128 columns) of B -> 32 KB/stage, 5-6 stages; the
 //         leader CTA issues the MMAs for both, halving per-SM smem operand traffic.
-// AUX: the epilogue has an aux stream (GELU/dGELU/SwiGLU/dSwiGLU) -> 8 KB of staging per
-// epilogue warp (out0 out1 aux0 aux1); plain stores need 4 KB, and the freed 32 KB buys
-// one more operand stage (deeper TMA prefetch for the K = 4096 GEMMs).
+// AUX: the epilogue has an aux stream (GELU/dGELU/SwiGLU/dSwiGLU; compile-time split so
+// the plain-store variant carries none of the activation code).  Aux streams bypass
+// shared memory (aux_block), so every variant stages only its outputs: 2 x 2 KB per
+// epilogue warp, leaving room for 6 (CTA pair) / 4 (single CTA) operand stages.
 template <int CG, bool AUX>
 struct Cfg {
-  static constexpr int kEpiWarpBytes = (AUX ? 4 : 2) * kEpiBuf;
+  static constexpr int kEpiWarpBytes = 2 * kEpiBuf;
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
   static constexpr int kBRows = BN / CG;                 // B rows (n) staged per CTA
   static constexpr int kATileBytes = BM * BK * 2;        // 16 KB
   static constexpr int kBTileBytes = kBRows * BK * 2;    // 32 KB / 16 KB
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CG == 1 ? (AUX ? 3 : 4) : (AUX ? 5 : 6);
+  static constexpr int kStages = CG == 1 ? 4 : 6;
   static constexpr int kTilesBytes = kStages * kStageBytes;
   static constexpr int kTileM = BM * CG;                 // rows per (pair) tile
   static constexpr int kSmemBytes = 1024 + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
@@ -368,6 +371,17 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
   return t;
 }
 
+// Private "epilogue-native" layout of the aux streams (GELU: gelu'(h); SwiGLU: S | Q),
+// written by a forward epilogue and read only by the matching backward epilogue: 32 x 32
+// blocks, block (r/32, c/32) at ((r/32) * (W/32) + c/32) * 1024 elements (W = aux width);
+// inside a block, element (row l, col 8q + i) sits at q * 256 + l * 8 + i -- so
+// instruction q of a warp whose lane l owns row l reads/writes 512 contiguous bytes, with
+// no shared-memory staging.  Same byte size as row-major [rows, W].
+__device__ __forceinline__ uint4* aux_block(const Params& p, int width, int row0, int col) {
+  return reinterpret_cast<uint4*>(p.aux) +
+         ((size_t)(row0 >> 5) * (width >> 5) + (col >> 5)) * 128;
+}
+
 // Static persistent schedule: wave w hands tile w*nunits + slot to unit `unit`, with the
 // slot order reversed on odd waves ("snake").  With tiles numbered in descending cost
 // (weight-gradient groups sorted by their K = rows) this is the LPT-style balance a
@@ -379,22 +393,21 @@ __device__ __forceinline__ int sched_tile(int w, int unit, int nunits) {
 // SwiGLU epilogues (Mixtral experts).  W1|W3 are interleaved in blocks of 128 output
 // rows, so one 256-wide N tile holds the gate (cols 0..127) and up (cols 128..255)
 // projections of the same 128 hidden units.
-//   SWIGLU : H[rows, N] = [G | U] pre-activations (aux, kept for backward),
-//            C[rows, N/2] = silu(G) * U at hidden column nb*128 + j
-//   DSWIGLU: GEMM output dA[rows, N] (N = d_ff, hidden units); reads G, U from the
-//            interleaved H[rows, 2N] and writes dH = [dG | dU] into C[rows, 2N]
-// Each epilogue warp owns 32 rows and one half of the tile's hidden units; single-
-// buffered staging (4 x 2 KB per warp), next chunk's G/U loads overlap the current chunk.
-
-__device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const TileInfo& t,
+//   SWIGLU : C[rows, N/2] = silu(g) * u at hidden column nb*128 + j; AUX [rows, N] keeps
+//            the backward's factors S = silu(g) (gate column), Q = u silu'(g) (up column)
+//   DSWIGLU: GEMM output dA[rows, N] (N = d_ff, hidden units); reads S, Q from AUX
+//            [rows, 2N] and writes dH = [dG | dU] = [dA Q | dA S] into C[rows, 2N]
+// AUX uses the private blocked layout (aux_block), accessed straight from registers.
+// Each epilogue warp owns 32 rows and one half of the tile's hidden units; the output
+// staging is double-buffered (2 x 2 KB per warp).
+__device__ __forceinline__ void swiglu_epilogue(const Params& p, bool fwd, const TileInfo& t,
                                              int row0, int half, int lane, uint32_t tbase,
                                              uint64_t* tfull, uint32_t acc_phase,
-                                             uint64_t* tempty, uint8_t* wbuf, uint64_t* abar,
-                                             uint32_t& aphase, const CUtensorMap* map_c,
-                                             const CUtensorMap* map_x, int cg) {
-  const uint32_t s_out0 = smem_u32(wbuf), s_out1 = s_out0 + kEpiBuf;
-  const uint32_t s_aux0 = s_out0 + 2 * kEpiBuf, s_aux1 = s_out0 + 3 * kEpiBuf;
+                                             uint64_t* tempty, uint8_t* wbuf,
+                                             const CUtensorMap* map_c, int cg) {
+  const uint32_t s_out = smem_u32(wbuf);
   const int nchunks = fwd ? 2 : 4;  // 64 hidden units (fwd) / 128 hidden units (bwd) per warp
+  const int auxw = fwd ? p.N : 2 * p.N;
   auto cols = [&](int c, int& gcol, int& ucol, int& hid) {
     if (fwd) {
       hid = t.nb * (BN / 2) + half * 64 + c * 32;              // Act column
@@ -407,13 +420,17 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
       ucol = gcol + 128;
     }
   };
-  if (!fwd && lane == 0) {  // first chunk's pre-activations
+  uint4 sn[4], qn[4];  // backward: next chunk's S and Q (in flight during this chunk)
+  if (!fwd) {
     int g, u, h;
     cols(0, g, u, h);
-    fence_async_smem();
-    mbar_expect_tx(abar, 2 * kEpiBuf);
-    tma_load_2d(wbuf + 2 * kEpiBuf, map_x, abar, g, row0);
-    tma_load_2d(wbuf + 3 * kEpiBuf, map_x, abar, u, row0);
+    const uint4* ps = aux_block(p, auxw, row0, g) + lane;
+    const uint4* pq = aux_block(p, auxw, row0, u) + lane;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sn[q] = ld_nc_v4(ps + q * 32);
+      qn[q] = ld_nc_v4(pq + q * 32);
+    }
   }
   mbar_wait(tfull, acc_phase);
   tc_fence_after();
@@ -436,85 +453,85 @@ __device__ __noinline__ void swiglu_epilogue(const Params& p, bool fwd, const Ti
       __syncwarp();
       if (lane == 0) tmem_release(tempty, cg);
     }
-    float g[32], u[32];
     if (fwd) {
-#pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        g[q] = __uint_as_float(va[q]);
-        u[q] = __uint_as_float(vb[q]);
-      }
-    } else {
-      mbar_wait(abar, aphase);
-      aphase ^= 1;
+      // out buffer c & 1: the store issued two chunks ago (previous tile) must be done
+      if (lane == 0) bulk_wait_read<1>();
+      __syncwarp();
+      uint4* ps = aux_block(p, auxw, row0, gcol) + lane;
+      uint4* pq = aux_block(p, auxw, row0, ucol) + lane;
+      const uint32_t so = s_out + (c & 1) * kEpiBuf;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        bf16x8_to_f32(ld_shared_v4(s_aux0 + stg_off(lane, q)), g + 8 * q);
-        bf16x8_to_f32(ld_shared_v4(s_aux1 + stg_off(lane, q)), u + 8 * q);
-      }
-    }
-    if (lane == 0) bulk_wait_read<0>();  // staging buffers free again
-    __syncwarp();
-    if (!fwd && c + 1 < nchunks && lane == 0) {
-      int g2, u2, h2;
-      cols(c + 1, g2, u2, h2);
-      fence_async_smem();
-      mbar_expect_tx(abar, 2 * kEpiBuf);
-      tma_load_2d(wbuf + 2 * kEpiBuf, map_x, abar, g2, row0);
-      tma_load_2d(wbuf + 3 * kEpiBuf, map_x, abar, u2, row0);
-    }
-    if (fwd) {
-      // aux keeps the backward's factors, not the pre-activations:
-      //   S = silu(g) (gate column), Q = u * silu'(g) (up column); act = S * u
-      float a[32];
+        float a[8], sv[8], qv[8];
 #pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        // packed: sg = (1 + tanh(g/2)) / 2, S = g sg, act = S u, Q = u sg (1 + g (1 - sg))
-        const float2 g2 = make_float2(g[q], g[q + 1]), u2 = make_float2(u[q], u[q + 1]);
-        const float2 h2 = mul2(g2, splat2(0.5f));
-        const float2 t2 = make_float2(tanh_fast(h2.x), tanh_fast(h2.y));
-        const float2 sg = fma2(t2, splat2(0.5f), splat2(0.5f));
-        const float2 om = fma2(t2, splat2(-0.5f), splat2(0.5f));
-        const float2 sl = mul2(g2, sg);
-        const float2 a2 = mul2(sl, u2);
-        const float2 q2 = mul2(mul2(u2, sg), fma2(g2, om, splat2(1.f)));
-        a[q] = a2.x;
-        a[q + 1] = a2.y;
-        u[q] = q2.x;
-        u[q + 1] = q2.y;
-        g[q] = sl.x;
-        g[q + 1] = sl.y;
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        st_shared_v4(s_aux0 + stg_off(lane, q), f32_to_bf16x8(g + 8 * q));
-        st_shared_v4(s_aux1 + stg_off(lane, q), f32_to_bf16x8(u + 8 * q));
-        st_shared_v4(s_out0 + stg_off(lane, q), f32_to_bf16x8(a + 8 * q));
+        for (int i = 0; i < 8; i += 2) {
+          // packed: sg = (1 + tanh(g/2)) / 2, S = g sg, act = S u, Q = u sg (1 + g (1 - sg))
+          const int j = 8 * q + i;
+          const float2 g2 = make_float2(__uint_as_float(va[j]), __uint_as_float(va[j + 1]));
+          const float2 u2 = make_float2(__uint_as_float(vb[j]), __uint_as_float(vb[j + 1]));
+          const float2 h2 = mul2(g2, splat2(0.5f));
+          const float2 t2 = make_float2(tanh_fast(h2.x), tanh_fast(h2.y));
+          const float2 sg = fma2(t2, splat2(0.5f), splat2(0.5f));
+          const float2 om = fma2(t2, splat2(-0.5f), splat2(0.5f));
+          const float2 sl = mul2(g2, sg);
+          const float2 a2 = mul2(sl, u2);
+          const float2 q2 = mul2(mul2(u2, sg), fma2(g2, om, splat2(1.f)));
+          a[i] = a2.x;
+          a[i + 1] = a2.y;
+          sv[i] = sl.x;
+          sv[i + 1] = sl.y;
+          qv[i] = q2.x;
+          qv[i + 1] = q2.y;
+        }
+        st_v4(ps + q * 32, f32_to_bf16x8(sv));
+        st_v4(pq + q * 32, f32_to_bf16x8(qv));
+        st_shared_v4(so + stg_off(lane, q), f32_to_bf16x8(a));
       }
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_2d(map_x, wbuf + 2 * kEpiBuf, gcol, row0);
-        tma_store_2d(map_x, wbuf + 3 * kEpiBuf, ucol, row0);
-        tma_store_2d(map_c, wbuf, hid, row0);
+        tma_store_2d(map_c, wbuf + (c & 1) * kEpiBuf, hid, row0);
         bulk_commit();
       }
     } else {
-      float dg[32], du[32];
-#pragma unroll
-      for (int q = 0; q < 32; q += 2) {
-        // g holds S = silu(g), u holds Q
-        const float2 da = make_float2(__uint_as_float(va[q]), __uint_as_float(va[q + 1]));
-        const float2 a = mul2(da, make_float2(g[q], g[q + 1]));
-        const float2 b = mul2(da, make_float2(u[q], u[q + 1]));
-        du[q] = a.x;
-        du[q + 1] = a.y;
-        dg[q] = b.x;
-        dg[q + 1] = b.y;
-      }
+      uint4 sc[4], qc[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        st_shared_v4(s_out0 + stg_off(lane, q), f32_to_bf16x8(dg + 8 * q));
-        st_shared_v4(s_out1 + stg_off(lane, q), f32_to_bf16x8(du + 8 * q));
+        sc[q] = sn[q];
+        qc[q] = qn[q];
+      }
+      if (c + 1 < nchunks) {
+        int g2, u2, h2;
+        cols(c + 1, g2, u2, h2);
+        const uint4* ps = aux_block(p, auxw, row0, g2) + lane;
+        const uint4* pq = aux_block(p, auxw, row0, u2) + lane;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          sn[q] = ld_nc_v4(ps + q * 32);
+          qn[q] = ld_nc_v4(pq + q * 32);
+        }
+      }
+      // both staging buffers are rewritten: the previous chunk's two stores must be done
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float sf[8], qf[8], dg[8], du[8];
+        bf16x8_to_f32(sc[q], sf);
+        bf16x8_to_f32(qc[q], qf);
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float2 da = make_float2(__uint_as_float(va[8 * q + i]),
+                                        __uint_as_float(va[8 * q + i + 1]));
+          const float2 x = mul2(da, make_float2(qf[i], qf[i + 1]));
+          const float2 y = mul2(da, make_float2(sf[i], sf[i + 1]));
+          dg[i] = x.x;
+          dg[i + 1] = x.y;
+          du[i] = y.x;
+          du[i + 1] = y.y;
+        }
+        st_shared_v4(s_out + stg_off(lane, q), f32_to_bf16x8(dg));
+        st_shared_v4(s_out + kEpiBuf + stg_off(lane, q), f32_to_bf16x8(du));
       }
       fence_async_smem();
       __syncwarp();
@@ -542,8 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint64_t* aux_bar = tempty_bar + 2;  // [epilogue warps][2 buffers]
-  uint32_t* s_tmem = (uint32_t*)(aux_bar + 2 * kEpiWarps);
+  uint32_t* s_tmem = (uint32_t*)(tempty_bar + 2);
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
@@ -591,7 +607,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], kEpiWarps * CG);  // one arrival per epilogue warp of each CTA
     }
-    for (int s = 0; s < 2 * kEpiWarps; ++s) mbar_init(&aux_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -699,9 +714,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;           // column half of the tile this warp owns
     uint8_t* wbuf = s_epi + ew * C::kEpiWarpBytes;
     const uint32_t out_s = smem_u32(wbuf);                 // out0, out1
-    const uint32_t aux_s = smem_u32(wbuf + 2 * kEpiBuf);   // aux0, aux1
-    uint64_t* my_aux_bar = aux_bar + ew * 2;
-    uint32_t aux_phase[2] = {0, 0};
     const bool gelu = AUX && p.epilogue == LZ_EPI_GELU, dgelu = AUX && p.epilogue == LZ_EPI_DGELU;
     const bool swiglu = AUX && p.epilogue == LZ_EPI_SWIGLU;
     const bool dswiglu = AUX && p.epilogue == LZ_EPI_DSWIGLU;
@@ -714,99 +726,106 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
-      if (dgelu && lane == 0) {
-        // prefetch the first two pre-activation chunks of this tile
-        fence_async_smem();
-        for (int c = 0; c < 2; ++c) {
-          mbar_expect_tx(&my_aux_bar[c], kEpiBuf);
-          tma_load_2d(wbuf + (2 + c) * kEpiBuf, &map_x, &my_aux_bar[c], col0 + c * kEpiCols, row0);
-        }
-      }
       if (swiglu || dswiglu) {
         swiglu_epilogue(p, swiglu, t, row0, half, lane, tmem_base + ((uint32_t)(quad * 32) << 16) +
                         acc * kAccCols, &tfull_bar[acc], acc_phase, &tempty_bar[acc], wbuf,
-                        my_aux_bar, aux_phase[0], &map_c, &map_x, CG);
+                        &map_c, CG);
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
         continue;
       }
-      mbar_wait(&tfull_bar[acc], acc_phase);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols +
-                             half * (BN / (kEpiWarps / 4));
+      // One instantiation per epilogue kind, so each has its own register allocation (the
+      // dGELU aux prefetch registers are not live in the GELU path and vice versa).
+      auto plain_tile = [&](auto kind) {
+        constexpr int K = decltype(kind)::value;   // 0 store, 1 GELU, 2 dGELU
+        // GELU / dGELU aux = gelu'(h) in the private blocked layout (aux_block): lane l
+        // of the warp owning rows row0..row0+31 touches 16 B per instruction at
+        // consecutive addresses -> 512 B coalesced accesses, no smem staging, no TMA
+        const uint4* aux_rd = nullptr;
+        uint4 hnext[4];
+        if constexpr (K == 2) {
+          aux_rd = aux_block(p, p.N, row0, col0) + lane;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) hnext[q] = ld_nc_v4(aux_rd + q * 32);
+        }
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols +
+                               half * (BN / (kEpiWarps / 4));
 #pragma unroll 1
-      for (int c = 0; c < kChunks; ++c) {
-        const int b = c & 1;
-        uint32_t v[32];
-        if (t.nk > 0) {
-          tmem_ld32(taddr + c * kEpiCols, v);
-        } else {
+        for (int c = 0; c < kChunks; ++c) {
+          const int b = c & 1;
+          uint32_t v[32];
+          if (t.nk > 0) {
+            tmem_ld32(taddr + c * kEpiCols, v);
+          } else {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = 0u;
-        }
-        if (c == kChunks - 1) {
-          // accumulator fully read: hand TMEM back to the MMA issuer early
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tmem_release(&tempty_bar[acc], CG);
-        }
-        float f[32];
+            for (int q = 0; q < 32; ++q) v[q] = 0u;
+          }
+          if (c == kChunks - 1) {
+            // accumulator fully read: hand TMEM back to the MMA issuer early
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tmem_release(&tempty_bar[acc], CG);
+          }
+          float f[32];
 #pragma unroll
-        for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
-        if (dgelu) {
-          // aux = gelu'(h) stored by the forward epilogue
-          mbar_wait(&my_aux_bar[b], aux_phase[b]);
-          aux_phase[b] ^= 1;
+          for (int q = 0; q < 32; ++q) f[q] = __uint_as_float(v[q]);
+          if constexpr (K == 2) {
+            // dA * gelu'(h) (aux loaded during the previous chunk)
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            float h[8];
-            bf16x8_to_f32(ld_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q)), h);
+            for (int q = 0; q < 4; ++q) {
+              float h[8];
+              bf16x8_to_f32(hnext[q], h);
 #pragma unroll
-            for (int i = 0; i < 8; i += 2) {
-              const float2 m = mul2(make_float2(f[8 * q + i], f[8 * q + i + 1]),
-                                    make_float2(h[i], h[i + 1]));
-              f[8 * q + i] = m.x;
-              f[8 * q + i + 1] = m.y;
+              for (int i = 0; i < 8; i += 2) {
+                const float2 m = mul2(make_float2(f[8 * q + i], f[8 * q + i + 1]),
+                                      make_float2(h[i], h[i + 1]));
+                f[8 * q + i] = m.x;
+                f[8 * q + i + 1] = m.y;
+              }
+            }
+            if (c + 1 < kChunks) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) hnext[q] = ld_nc_v4(aux_rd + (c + 1) * 128 + q * 32);
             }
           }
-        }
-        // the store that used buffer b (chunk c-2) must have finished reading smem
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        if (dgelu && c + 2 < kChunks && lane == 0) {
-          fence_async_smem();
-          mbar_expect_tx(&my_aux_bar[b], kEpiBuf);
-          tma_load_2d(wbuf + (2 + b) * kEpiBuf, &map_x, &my_aux_bar[b],
-                      col0 + (c + 2) * kEpiCols, row0);
-        }
-        if (gelu) {
-          float dg[32];
+          // the store that used buffer b (chunk c-2) must have finished reading smem
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          if constexpr (K == 1) {
+            uint4* aux_wr = aux_block(p, p.N, row0, col0 + c * kEpiCols) + lane;
 #pragma unroll
-          for (int q = 0; q < 32; q += 2) {
-            float2 y2, d2;
-            gelu_and_grad2(make_float2(f[q], f[q + 1]), y2, d2);
-            f[q] = y2.x;
-            f[q + 1] = y2.y;
-            dg[q] = d2.x;
-            dg[q + 1] = d2.y;
+            for (int q = 0; q < 4; ++q) {
+              float dg[8];
+#pragma unroll
+              for (int i = 0; i < 8; i += 2) {
+                float2 y2, d2;
+                gelu_and_grad2(make_float2(f[8 * q + i], f[8 * q + i + 1]), y2, d2);
+                f[8 * q + i] = y2.x;
+                f[8 * q + i + 1] = y2.y;
+                dg[i] = d2.x;
+                dg[i + 1] = d2.y;
+              }
+              st_v4(aux_wr + q * 32, f32_to_bf16x8(dg));
+            }
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            st_shared_v4(aux_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(dg + 8 * q));
+            st_shared_v4(out_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&map_c, wbuf + b * kEpiBuf, col0 + c * kEpiCols, row0);
+            bulk_commit();
+          }
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          st_shared_v4(out_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&map_c, wbuf + b * kEpiBuf, col0 + c * kEpiCols, row0);
-          if (gelu) tma_store_2d(&map_x, wbuf + (2 + b) * kEpiBuf, col0 + c * kEpiCols, row0);
-          bulk_commit();
-        }
-      }
+      };
+      if (gelu) plain_tile(std::integral_constant<int, 1>{});
+      else if (dgelu) plain_tile(std::integral_constant<int, 2>{});
+      else plain_tile(std::integral_constant<int, 0>{});
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;

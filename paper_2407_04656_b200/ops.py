@@ -163,6 +163,22 @@ def grouped_gemm_rows(A, B, off, C, *, b_major=_lib.LZ_K_MAJOR, epilogue=_lib.LZ
     return C
 
 
+def aux_rows(aux: torch.Tensor) -> torch.Tensor:
+    """The epilogue aux streams (GELU: gelu'(h); SwiGLU: S | Q -- written by a forward
+    epilogue, read only by the matching backward one) are stored in a private
+    32x32-blocked layout that keeps the epilogue's global accesses coalesced without
+    shared-memory staging (csrc/gemm.cu aux_block).  Row-major view of it (tests /
+    debugging).  aux: [rows, W], rows % 32 == 0, W % 32 == 0."""
+    R, N = aux.shape
+    return aux.reshape(R // 32, N // 32, 4, 32, 8).permute(0, 3, 1, 2, 4).reshape(R, N)
+
+
+def aux_blocked(rows_major: torch.Tensor) -> torch.Tensor:
+    """Inverse of :func:`aux_rows`."""
+    R, N = rows_major.shape
+    return rows_major.reshape(R // 32, 32, N // 32, 4, 8).permute(0, 2, 3, 1, 4).reshape(R, N)
+
+
 def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0, c_group_rows: int = 0,
                        c_row_offset: int = 0):
     """C_g = A[off[g]:off[g+1]]^T . B[off[g]:off[g+1]]; A [rows, M], B [rows, N].

@@ -88,14 +88,21 @@ def test_gelu_and_dgelu_epilogues(cg):
     ops.grouped_gemm_rows(A, B2, off_t, dH, b_major=_lib.LZ_MN_MAJOR,
                           epilogue=_lib.LZ_EPI_DGELU, aux=D)
     torch.cuda.synchronize()
+    Drows = ops.aux_rows(D)   # the aux stream is in the private blocked layout
     for g in range(G):
         sl = slice(off[g], off[g + 1])
         pre = (A[sl].float() @ B[g].float().t()).requires_grad_(True)
         act = torch.nn.functional.gelu(pre, approximate="tanh")
         act.backward(torch.ones_like(act))
         _close(Act[sl], act.detach(), rtol=2e-2)
-        _close(D[sl], pre.grad, rtol=2e-2)
-        _close(dH[sl], (A[sl].float() @ B2[g].float()) * D[sl].float(), rtol=2e-2)
+        _close(Drows[sl], pre.grad, rtol=2e-2)
+        _close(dH[sl], (A[sl].float() @ B2[g].float()) * Drows[sl].float(), rtol=2e-2)
+
+
+def test_gelu_aux_layout_roundtrip():
+    x = torch.arange(64 * 96, dtype=torch.float32).view(64, 96)
+    from paper_2407_04656_b200 import ops as O
+    assert torch.equal(O.aux_rows(O.aux_blocked(x)), x)
 
 
 @pytest.mark.parametrize("sizes,M,N", [([128], 256, 256), ([64, 0, 192, 128], 256, 512),
@@ -173,6 +180,7 @@ def test_swiglu_epilogues(cg):
     ops.grouped_gemm_rows(X, B2, off_t, dH, b_major=_lib.LZ_MN_MAJOR,
                           epilogue=_lib.LZ_EPI_DSWIGLU, aux=H)
     torch.cuda.synchronize()
+    Hrows = ops.aux_rows(H)   # private blocked layout -> row-major view
     for g in range(G):
         sl = slice(off[g], off[g + 1])
         xg = X[sl].float()
@@ -181,7 +189,7 @@ def test_swiglu_epilogues(cg):
         act = torch.nn.functional.silu(gate) * up
         dA = xg @ B2[g].float()
         act.backward(dA)
-        Hi = H[sl].view(-1, F // 128, 2, 128)
+        Hi = Hrows[sl].view(-1, F // 128, 2, 128)
         S, Q = Hi[:, :, 0].reshape(-1, F), Hi[:, :, 1].reshape(-1, F)
         sg = torch.sigmoid(gate.detach())
         _close(Act[sl], act.detach(), rtol=2e-2)
