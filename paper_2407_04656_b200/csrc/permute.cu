@@ -449,30 +449,192 @@ __global__ void __launch_bounds__(256, 2) router_wgrad_partial(const float* __re
     part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
 }
 
-// 16 lanes per output element, each summing a strided subset of the block partials,
-// then a 16-lane shuffle reduction (fixed order: deterministic).
+// Tensor-core variant: dWg^T[col, e] = sum_t x[t, col] dl[t, e] as mma.sync m16n8k16
+// (M = 16 columns, N = 8 experts, K = 16 tokens).  The block stages 16 tokens x 1024
+// columns of x (cp.async, double-buffered) and their dlogits; ldmatrix.trans turns the
+// token-major x tile into A fragments; dlogits enter as a bf16 hi + lo split (the
+// product keeps ~16 mantissa bits, as in the dispatch backward).  Warp w owns columns
+// [w*256, +256) of the block's slice and 16 experts (two n8 tiles).  One pass over x
+// per 16-expert group; per-block partials as in the FMA kernel.
+constexpr int kRwTok = 16, kRwCols = 1024, kRwPad = 8, kRwStages = 3;
+constexpr int kRwRow = kRwCols + kRwPad;                    // bf16 elements per smem row
+constexpr int kRwSmem = kRwStages * (kRwTok * kRwRow * 2 + kRwTok * 16 * 4);
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(pred ? 16 : 0));
+}
+__global__ void __launch_bounds__(128, 2) router_wgrad_tc(const float* __restrict__ dlog,
+                                                       const __nv_bfloat16* __restrict__ x,
+                                                       int Tn, int d, int E,
+                                                       float* __restrict__ part,
+                                                       float* __restrict__ part_bias) {
+  extern __shared__ __align__(16) uint8_t rw_smem[];
+  __nv_bfloat16* s_x = reinterpret_cast<__nv_bfloat16*>(rw_smem);  // [stages][16][kRwRow]
+  float* s_dl = reinterpret_cast<float*>(rw_smem + kRwStages * kRwTok * kRwRow * 2);
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nblk = gridDim.x;
+  const int cbase = blockIdx.y * kRwCols;                 // block column slice
+  const int ncols = min(kRwCols, d - cbase);
+  const int e0 = blockIdx.z * 16;
+  const long per = ((long)(Tn + nblk - 1) / nblk + kRwTok - 1) / kRwTok * kRwTok;
+  const long t_begin = (long)blockIdx.x * per;
+  const long t_end = min((long)Tn, t_begin + per);
+  const uint32_t sx0 = (uint32_t)__cvta_generic_to_shared(s_x);
+  // staging assignment (computed once): thread -> 16-byte piece cc of rows ti0, +rstep, ..
+  const int pr = ncols / 8;                     // pieces per row (<= 128 = blockDim.x)
+  const int rstep = blockDim.x / pr;
+  const int ti0 = threadIdx.x < rstep * pr ? threadIdx.x / pr : kRwTok;  // idle if surplus
+  const int cc = threadIdx.x % pr;
+  auto stage = [&](int buf, long tt) {
+    // x rows: 16 tokens x ncols bf16 in 16-byte pieces; dlogits 16 x 16 fp32
+    for (int ti = ti0; ti < kRwTok; ti += rstep) {
+      const long t = tt + ti;
+      const bool ok = t < t_end;
+      cp_async16(sx0 + (uint32_t)(((buf * kRwTok + ti) * kRwRow + cc * 8) * 2),
+                 x + (ok ? t : 0) * d + cbase + cc * 8, ok);
+    }
+    const uint32_t sdl0 = (uint32_t)__cvta_generic_to_shared(s_dl);
+    for (int q = threadIdx.x; q < kRwTok * 16; q += blockDim.x) {
+      const int ti = q / 16, ei = q % 16;
+      const long t = tt + ti;
+      const bool ok = t < t_end && e0 + ei < E;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                       sdl0 + (uint32_t)(((buf * kRwTok + ti) * 16 + ei) * 4)),
+                   "l"(dlog + (ok ? t * E + e0 + ei : 0)), "r"(ok ? 4 : 0));
+    }
+    asm volatile("cp.async.commit_group;");
+  };
+  float acc[16][2][4];
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[m][n][q] = 0.f;
+  float bacc = 0.f;
+  const int wcol = warp * 256;                            // warp's columns in the slice
+  const bool active = wcol < ncols;
+  // kRwStages-deep cp.async ring: steps i+1 .. i+kRwStages-1 are in flight while step i
+  // is consumed (one commit group per step, empty groups past the end keep the count)
+  const long nsteps = t_end > t_begin ? (t_end - t_begin + kRwTok - 1) / kRwTok : 0;
+#pragma unroll
+  for (int i = 0; i < kRwStages - 1; ++i) {
+    if (i < nsteps) stage(i, t_begin + (long)i * kRwTok);
+    else asm volatile("cp.async.commit_group;");
+  }
+  for (long i = 0; i < nsteps; ++i) {
+    const int buf = (int)(i % kRwStages);
+    const long tt = t_begin + i * kRwTok;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kRwStages - 2) : "memory");
+    __syncthreads();
+    {
+      const long j = i + kRwStages - 1;   // restage the buffer consumed at step i - 1
+      if (j < nsteps) stage((int)(j % kRwStages), t_begin + j * kRwTok);
+      else asm volatile("cp.async.commit_group;");
+    }
+    const float* dl = s_dl + buf * kRwTok * 16;
+    if (blockIdx.y == 0 && threadIdx.x < 16)
+      for (int ti = 0; ti < kRwTok; ++ti) bacc += dl[ti * 16 + threadIdx.x];
+    if (active) {
+      // B fragments (experts g and 8 + g; tokens 2t4, 2t4+1 and +8), hi / lo bf16
+      uint32_t bh[2][2], bl[2][2];
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int k0 = 2 * t4 + 8 * h;
+          const float v0 = dl[k0 * 16 + n * 8 + g], v1 = dl[(k0 + 1) * 16 + n * 8 + g];
+          bh[n][h] = bf16pair(v0, v1);
+          const float h0 = __uint_as_float(bh[n][h] << 16);
+          const float h1 = __uint_as_float(bh[n][h] & 0xffff0000u);
+          bl[n][h] = bf16pair(v0 - h0, v1 - h1);
+        }
+      // A fragments: ldmatrix.x4.trans of the 16 tokens x 16 columns submatrix
+      const int mi = lane >> 3, r = lane & 7;
+      const uint32_t abase = sx0 + (uint32_t)(((buf * kRwTok + (mi >> 1) * 8 + r) * kRwRow +
+                                               wcol + (mi & 1) * 8) * 2);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        if (wcol + m * 16 >= ncols) break;
+        uint32_t a0, a1, a2, a3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                     : "r"(abase + m * 32));
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          mma16816(acc[m][n], a0, a1, a2, a3, bh[n][0], bh[n][1]);
+          mma16816(acc[m][n], a0, a1, a2, a3, bl[n][0], bl[n][1]);
+        }
+      }
+    }
+    (void)tt;
+  }
+  // partial[blk][e][col]: C fragment rows = columns (g, g + 8), cols = experts (2t4, +1)
+  if (active) {
+    float* pb = part + (long)blockIdx.x * E * d;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int c = cbase + wcol + m * 16 + g;
+      if (wcol + m * 16 >= ncols) break;
+#pragma unroll
+      for (int n = 0; n < 2; ++n) {
+        const int e = e0 + n * 8 + 2 * t4;
+        if (e < E) {
+          pb[(long)e * d + c] = acc[m][n][0];
+          pb[(long)e * d + c + 8] = acc[m][n][2];
+        }
+        if (e + 1 < E) {
+          pb[(long)(e + 1) * d + c] = acc[m][n][1];
+          pb[(long)(e + 1) * d + c + 8] = acc[m][n][3];
+        }
+      }
+    }
+  }
+  if (blockIdx.y == 0 && threadIdx.x < 16 && e0 + threadIdx.x < E)
+    part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
+}
+
+// Block = 8 warps x 32 consecutive output elements (coalesced 128-byte loads); warp w
+// sums partials w, w + 8, ... and the 8 warp sums are added in a fixed order through
+// shared memory (deterministic).  The trailing ceil(E/32) blocks reduce the bias partials.
 __global__ void __launch_bounds__(256) router_wgrad_reduce(const float* __restrict__ part,
                                                            const float* __restrict__ part_bias,
                                                            int nblk, int d, int E,
                                                            float* __restrict__ dwg,
                                                            float* __restrict__ dbias) {
+  __shared__ float s_sum[8][33];
   const long n = (long)E * d;
-  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long i = gid >> 4;
-  const int sub = threadIdx.x & 15;
-  float s = 0.f, sb = 0.f;
-  if (i < n)
-    for (int b = sub; b < nblk; b += 16) s += part[(long)b * n + i];
-  if (dbias && i < E)
-    for (int b = sub; b < nblk; b += 16) sb += part_bias[(long)b * E + i];
-#pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    sb += __shfl_xor_sync(0xffffffffu, sb, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long nmain = (n + 31) / 32;
+  const bool bias_blk = blockIdx.x >= nmain;
+  const long i = (bias_blk ? blockIdx.x - nmain : blockIdx.x) * 32 + lane;
+  const long stride = bias_blk ? E : n;
+  const float* src = bias_blk ? part_bias : part;
+  const bool ok = bias_blk ? (dbias != nullptr && i < E) : i < n;
+  float s = 0.f;
+  if (ok) {
+    int b = warp;
+    for (; b + 24 < nblk; b += 32) {   // 4 independent loads in flight per iteration
+      const float v0 = __ldg(src + (long)b * stride + i);
+      const float v1 = __ldg(src + (long)(b + 8) * stride + i);
+      const float v2 = __ldg(src + (long)(b + 16) * stride + i);
+      const float v3 = __ldg(src + (long)(b + 24) * stride + i);
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; b < nblk; b += 8) s += __ldg(src + (long)b * stride + i);
   }
-  if (sub == 0 && i < n) {
-    dwg[i] = s;
-    if (dbias && i < E) dbias[i] = sb;
+  s_sum[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float t = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += s_sum[w][lane];
+    if (bias_blk) dbias[i] = t;
+    else dwg[i] = t;
   }
 }
 
@@ -645,7 +807,17 @@ extern "C" lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe,
                            E, renorm, dx, dlogits, stream);
 }
 
-static int wgrad_nblk(int Tn) {
+// tensor-core path: d a multiple of 256 (whole warp column blocks); one block per SM
+// per (column slice, expert group); else the FMA path with 2 blocks per SM
+static bool wgrad_tc(int d) { return d % 256 == 0; }
+static int wgrad_nblk(int Tn, int d, int E) {
+  if (wgrad_tc(d)) {
+    const int slices = ((d + kRwCols - 1) / kRwCols) * ((E + 15) / 16);
+    int n = (2 * lzh::num_sms() + slices - 1) / slices;  // 2 blocks per SM
+    const int steps = (Tn + kRwTok - 1) / kRwTok;
+    if (n > steps) n = steps;
+    return n < 1 ? 1 : n;
+  }
   int n = 2 * lzh::num_sms();
   long per = (Tn + n - 1) / n;
   if (per < 64) n = (Tn + 63) / 64;
@@ -653,7 +825,7 @@ static int wgrad_nblk(int Tn) {
 }
 
 extern "C" size_t lz_router_wgrad_ws_bytes(int Tn, int d, int E) {
-  const size_t nblk = (size_t)wgrad_nblk(Tn);
+  const size_t nblk = (size_t)wgrad_nblk(Tn, d, E);
   return nblk * (size_t)E * d * sizeof(float) + nblk * (size_t)E * sizeof(float) + 256;
 }
 
@@ -669,17 +841,30 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
   }
   if (!dlogits || !x || !ws) return LZ_ERR_ARG;
   if (ws_bytes < lz_router_wgrad_ws_bytes(Tn, d, E)) return LZ_ERR_WORKSPACE;
-  const int nblk = wgrad_nblk(Tn);
+  const int nblk = wgrad_nblk(Tn, d, E);
   float* part = (float*)ws;
   float* part_bias = part + (size_t)nblk * E * d;
-  dim3 grid(nblk, (d + 1023) / 1024, (E + kWgE - 1) / kWgE);
-  router_wgrad_partial<<<grid, 256, 0, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
-                                            part_bias);
+  if (wgrad_tc(d)) {
+    static bool attr = false;
+    if (!attr) {
+      if (cudaFuncSetAttribute(router_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kRwSmem) != cudaSuccess)
+        return lzh::check_launch();
+      attr = true;
+    }
+    dim3 grid(nblk, (d + kRwCols - 1) / kRwCols, (E + 15) / 16);
+    router_wgrad_tc<<<grid, 128, kRwSmem, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
+                                               part_bias);
+  } else {
+    dim3 grid(nblk, (d + 1023) / 1024, (E + kWgE - 1) / kWgE);
+    router_wgrad_partial<<<grid, 256, 0, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
+                                              part_bias);
+  }
   lz_status st = lzh::check_launch();
   if (st != LZ_OK) return st;
   const long n = (long)E * d;
-  router_wgrad_reduce<<<(int)((16 * n + 255) / 256), 256, 0, s>>>(part, part_bias, nblk, d, E,
-                                                                  dwg, dbias);
+  router_wgrad_reduce<<<(int)((n + 31) / 32 + (E + 31) / 32), 256, 0, s>>>(part, part_bias, nblk,
+                                                                          d, E, dwg, dbias);
   return lzh::check_launch();
 }
 

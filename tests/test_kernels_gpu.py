@@ -131,6 +131,19 @@ def test_dispatch_bwd_and_router_grads(renorm):
     _close(db, dlog.cpu().sum(0), rtol=1e-4, atol_scale=1e-4)
 
 
+@pytest.mark.parametrize("Tn,d,E", [(1000, 1024, 16), (333, 2048, 8), (4099, 4096, 40),
+                                     (100, 96, 5), (17, 256, 64)])
+def test_router_wgrad_shapes(Tn, d, E):
+    """dWg = dlogits^T x and dbias = sum_t dlogits: tensor-core path (d % 256 == 0, any
+    E, ragged token counts) and the FMA path, against fp32 torch."""
+    gen = torch.Generator().manual_seed(11)
+    x = torch.randn(Tn, d, generator=gen).bfloat16()
+    dlog = torch.randn(Tn, E, generator=gen) * 1e-2
+    dwg, db = ops.router_wgrad(dlog.cuda(), x.cuda())
+    _close(dwg, dlog.t() @ x.float(), rtol=1e-4, atol_scale=1e-4)
+    _close(db, dlog.sum(0), rtol=1e-4, atol_scale=1e-4)
+
+
 def test_copy_segments():
     gen = torch.Generator().manual_seed(8)
     d = 256
