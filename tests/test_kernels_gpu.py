@@ -37,7 +37,8 @@ def test_gate_topk_exact_ids(Tn, E, k, renorm):
 
 
 @pytest.mark.parametrize("Tn,d,E,k", [(4096, 1024, 16, 2), (1000, 512, 8, 2), (257, 2048, 64, 1),
-                                      (100, 4096, 8, 2)])
+                                      (100, 4096, 8, 2), (70000, 1024, 16, 2), (300, 96, 5, 1),
+                                      (513, 256, 40, 3)])
 def test_router_gate(Tn, d, E, k):
     g = torch.Generator().manual_seed(d)
     x = torch.randn(Tn, d, generator=g).bfloat16()
