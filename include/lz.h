@@ -228,11 +228,21 @@ lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void*
 /* GEMM variant: 2 = CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles; default),
  * 1 = single-CTA kernel (128-row tiles).  Returns the active value. */
 int lz_gemm_set_cta_group(int cta_group);
-/* Epilogue store path: 1 = registers -> global (no smem staging), 0 = swizzled smem
- * staging + TMA bulk-tensor stores (default).  Returns the active value. */
+/* Retained for ABI compatibility: the register -> global epilogue variants were measured
+ * 1.6-2x slower and removed; every call returns 0 (smem staging + TMA stores). */
 int lz_gemm_set_direct_epilogue(int on);
 /* Row alignment mode-0 group segments must have for the active variant (128 or 256). */
 int lz_gemm_row_align(void);
+
+/* ---------------------------------------------------------- recovery probability */
+
+/* Number of failed-node sets F (|F| = k_failed, nodes 0..n_nodes-1) that leave every
+ * expert with a surviving holder: holders[e] = bit mask of the nodes holding expert e
+ * (E <= 1024, n_nodes <= 63).  *good (device u64) is overwritten asynchronously.
+ * recovery probability = good / C(n_nodes, k_failed).  Replaces the Python enumeration
+ * of reliability.py:68-96 (recovery_probability_exact) without its 10^6-subset cap. */
+lz_status lz_recovery_count(const unsigned long long* holders, int E, int n_nodes, int k_failed,
+                            unsigned long long* good, void* stream);
 
 #ifdef __cplusplus
 }

@@ -255,6 +255,38 @@ def main() -> None:
                     "assignment": [list(a) for a in m.assignment],
                     "transfers": [[list(t.item), t.source, t.dest] for t in sched.transfers]})
     pl["rebalance"] = reb
+    # recovery probabilities of MRO plans (reliability.py:68-125)
+    from flexep.reliability import (recovery_probability_closed_form,
+                                    recovery_probability_exact)
+    rec = []
+    rng = random.Random(0x5EC0)
+    for _ in range(40):
+        E = rng.choice([4, 8, 16, 32])
+        n = rng.choice([3, 4, 6, 8, 12, 16])
+        c = -(-E // n) + rng.randint(0, 3)
+        f = rng.randint(1, min(3, n))
+        loads = [rng.randint(1, 1000) for _ in range(E)]
+        spec = ClusterSpec(n_nodes=n, slots_per_node=c, fault_threshold=f)
+        try:
+            alloc = allocate_replicas(loads, spec)
+            plan = build_mro_plan(alloc, spec)
+        except Exception:
+            continue
+        ks = sorted({0, 1, f, min(n, f + 1), n // 2, n})
+        ex = {}
+        for k in ks:
+            try:
+                fr = recovery_probability_exact(plan, k, enumeration_cap=10**6)
+                ex[str(k)] = [fr.numerator, fr.denominator]
+            except Exception:
+                pass
+        cf = {}
+        for r in range(n + 1):
+            fr = recovery_probability_closed_form(alloc, spec, r)
+            cf[str(r)] = [fr.numerator, fr.denominator]
+        rec.append({"E": E, "n": n, "c": c, "f": f, "loads": loads,
+                    "slots": [list(x) for x in plan.slots], "exact": ex, "closed_form": cf})
+    pl["recovery"] = rec
     with open(os.path.join(HERE, "placement_golden.json"), "w") as f:
         json.dump(pl, f, separators=(",", ":"))
     print("wrote golden vectors")
