@@ -233,8 +233,6 @@ def run_gpu(args, cfg):
     graph, graph_err = None, ""
     if args.no_graph:
         graph_err = "graphs disabled"
-    elif world > 1:
-        graph_err = "graph capture is used at N=1 only in this round"
     else:
         from paper_2407_04656_b200.graphs import GraphedStep
         try:
@@ -314,6 +312,9 @@ def run_gpu(args, cfg):
         with torch.no_grad():
             for pa, pb in zip(fresh.parameters(), layer.parameters()):
                 pa.copy_(pb)
+        # N > 1: keep the already rendezvoused symmetric buffers (no second collective
+        # allocation, and the old ones are never freed under a rank's feet)
+        fresh._symm, fresh._symm_group = layer._symm, layer._symm_group
         layer = fresh
         for _ in range(3):
             step(x, dout)

@@ -46,7 +46,9 @@ class GraphedStep:
             layer.zero_grad(set_to_none=True)
             g = torch.cuda.CUDAGraph()
             l0 = _lib.launch_count
-            with torch.cuda.graph(g, pool=pool):
+            # thread_local: other threads (the NCCL watchdog polling its events) keep
+            # running while this thread captures
+            with torch.cuda.graph(g, pool=pool, capture_error_mode="thread_local"):
                 out = layer(self.x[i])
                 if backward:
                     out.backward(self.dout[i])
