@@ -349,6 +349,10 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     stages = {k2: round(v / nb, 4) for k2, v in stage_breakdown(layer.stage_events).items()}
     layer.stage_events = None
+    stages_all = [stages]
+    if world > 1:
+        stages_all = [None] * world
+        dist.all_gather_object(stages_all, stages)
 
     # ---- e2e through the public API: pinned host input -> device, result -> host.
     # Each step's x and upstream gradient are copied H2D on a side stream one step ahead
@@ -437,6 +441,7 @@ def run_gpu(args, cfg):
             "gpu_launches": launches,
             "clocks": clk,
             "stages_ms_rank0": stages,
+            "stages_ms_per_rank": stages_all if world > 1 else None,
             "exchange": layer.exchange_mode(),
         }
         if world == 1 and not args.no_cpu_baseline:

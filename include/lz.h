@@ -152,6 +152,15 @@ lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, 
 lz_status lz_pack_p2p(const void* x, int Tn, int d, int k, const int32_t* dest_rank,
                       const int32_t* dest_row, const unsigned long long* peers, void* own, int E,
                       const int32_t* recv_m, const int32_t* recv_off, void* stream);
+/* As lz_pack_p2p, and records in the owner's return map (symmetric, int64 per receive
+ * row: ret_peers[owner][dest_row] = my_rank << 32 | ret_row[t*k + s]; own pad rows = -1)
+ * where each row must go back to -- consumed by lz_grouped_gemm_scatter.  With ret_row =
+ * the plan's send slot every (owner, expert) segment returns to a contiguous row range. */
+lz_status lz_pack_p2p_ret(const void* x, int Tn, int d, int k, const int32_t* dest_rank,
+                          const int32_t* dest_row, const unsigned long long* peers, void* own,
+                          int E, const int32_t* recv_m, const int32_t* recv_off,
+                          const unsigned long long* ret_peers, long long* ret_own, int my_rank,
+                          const int32_t* ret_row, void* stream);
 lz_status lz_combine_p2p(const unsigned long long* peers_y, const int32_t* dest_rank,
                          const int32_t* dest_row, const float* w, int Tn, int d, int k, void* out,
                          void* stream);
@@ -160,6 +169,14 @@ lz_status lz_combine_bwd_p2p(const void* dout, const unsigned long long* peers_y
                              const int32_t* dest_row, const float* w, int Tn, int d, int k,
                              float* dw, void* own_dy, int E, const int32_t* recv_m,
                              const int32_t* recv_off, void* stream);
+/* As lz_combine_bwd_p2p with y read locally: assignment p's expert output is row
+ * y_row[p] of this rank's return buffer y_ret (written by the owners'
+ * lz_grouped_gemm_scatter); dy rows still go to the owners' buffers. */
+lz_status lz_combine_bwd_p2p_ret(const void* dout, const void* y_ret, const int32_t* y_row,
+                                 const unsigned long long* peers_dy, const int32_t* dest_rank,
+                                 const int32_t* dest_row, const float* w, int Tn, int d, int k,
+                                 float* dw, void* own_dy, int E, const int32_t* recv_m,
+                                 const int32_t* recv_off, void* stream);
 lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe, const int32_t* dest_rank,
                               const int32_t* dest_row, int Tn, int d, int k, const float* probs,
                               const int32_t* idx, const float* dw, const void* wg, int E,
@@ -228,6 +245,21 @@ lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void*
 /* GEMM variant: 2 = CTA-pair kernel (tcgen05 cta_group::2, 256-row tiles; default),
  * 1 = single-CTA kernel (128-row tiles).  Returns the active value. */
 int lz_gemm_set_cta_group(int cta_group);
+/* Scatter variant of the mode-0 store GEMM (the multi-GPU expert FFN's last GEMM of each
+ * direction): output row r is written -- straight from the epilogue registers, over
+ * NVLink for remote ranks -- to row (ret_map[r] & 0xffffffff) of the buffer at
+ * ret_peers[ret_map[r] >> 32] (rows of N bf16); ret_map[r] < 0 marks a pad row.  C is
+ * not written (pass any valid [rows_total, N] buffer).  The rows return to the ranks that
+ * dispatched them, so the combine / dispatch-backward read their own memory.
+ * ret_peers (device) and ret_peers_host (host copy) hold the n_peers return buffers of
+ * ret_rows rows each; 32-row chunks returning to consecutive rows of one rank (n_peers <=
+ * 8) go out as TMA bulk-tensor stores, the rest as per-row stores. */
+lz_status lz_grouped_gemm_scatter(const void* A, const void* B, void* C, int G,
+                                  const int32_t* off, int rows_total, int N, int K, int b_major,
+                                  int num_sms, const long long* ret_map,
+                                  const unsigned long long* ret_peers,
+                                  const unsigned long long* ret_peers_host, int n_peers,
+                                  int ret_rows, void* stream);
 /* Retained for ABI compatibility: the register -> global epilogue variants were measured
  * 1.6-2x slower and removed; every call returns 0 (smem staging + TMA stores). */
 int lz_gemm_set_direct_epilogue(int on);

@@ -30,6 +30,12 @@ _SIGS = {
     "lz_shuffle_index": [_vp, _i, _i, _vp, _i, _vp, _vp, _vp, _vp, _sz, _vp],
     "lz_load_record": [_vp, _i, _i, _vp, _i, _vp, _vp],
     "lz_recovery_count": [_vp, _i, _i, _i, _vp, _vp],
+    "lz_pack_p2p_ret": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _i, _vp,
+                        _vp],
+    "lz_combine_bwd_p2p_ret": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp,
+                               _vp, _vp],
+    "lz_grouped_gemm_scatter": [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i,
+                                _i, _vp],
     "lz_gate_topk": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "lz_router_gate": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "lz_invert_permutation": [_vp, _i, _vp, _vp],
@@ -95,7 +101,8 @@ _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
             "lz_copy_segments": 1, "lz_combine": 1, "lz_combine_bwd": 1, "lz_dispatch_bwd": 1,
             "lz_router_wgrad": 2, "lz_grouped_gemm": 1, "lz_pack_p2p": 1, "lz_combine_p2p": 1,
             "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1, "lz_load_record": 1,
-            "lz_recovery_count": 1}
+            "lz_recovery_count": 1, "lz_pack_p2p_ret": 1, "lz_combine_bwd_p2p_ret": 1,
+            "lz_grouped_gemm_scatter": 1}
 launch_count = 0
 
 

@@ -65,14 +65,24 @@ class SymmetricRows:
         base = [self.h.get_remote_tensor(r, (nbuf, rows, d), torch.bfloat16).data_ptr()
                 for r in range(n)]
         stride = rows * d * 2
-        self.ptrs = torch.tensor([[b + i * stride for b in base] for i in range(nbuf)],
-                                 dtype=torch.int64, device=device)
+        self.host_ptrs = [[b + i * stride for b in base] for i in range(nbuf)]
+        self.ptrs = torch.tensor(self.host_ptrs, dtype=torch.int64, device=device)
+        # return map (int64 per receive row: source rank << 32 | source assignment), written
+        # by the senders' dispatch, read by the owner's scattering GEMM epilogue
+        self.ret = symm.empty((rows,), dtype=torch.int64, device=device)
+        self.hr = symm.rendezvous(self.ret, group)
+        self.ret_ptrs = torch.tensor(
+            [self.hr.get_remote_tensor(r, (rows,), torch.int64).data_ptr() for r in range(n)],
+            dtype=torch.int64, device=device)
 
     def buf(self, i: int) -> torch.Tensor:
         return self.t[i]
 
     def peers(self, i: int) -> torch.Tensor:
         return self.ptrs[i]
+
+    def peers_host(self, i: int) -> list[int]:
+        return self.host_ptrs[i]
 
     def barrier(self) -> None:
         self.h.barrier(channel=0)

@@ -320,6 +320,20 @@ struct Params {
   __nv_bfloat16* C;        // direct epilogue: output base and row stride (elements)
   __nv_bfloat16* aux;
   long ldc, ldx;
+  // scatter epilogue (store variant, mode 0): output row r goes to rank (ret_map[r] >> 32)
+  // at row (ret_map[r] & 0xffffffff) of its buffer ret_peers[rank] (row length N); -1 = pad
+  const long long* ret_map;
+  const unsigned long long* ret_peers;
+};
+
+// Per-rank tensor maps of the scatter GEMM's return buffers ([rows, N] bf16 each): a
+// 32-row chunk whose rows return to consecutive rows of one rank (the common case: the
+// dispatch lays every (owner, expert) segment out contiguously on the source) is one TMA
+// store into that rank's buffer, over NVLink for remote ranks.
+constexpr int kMaxRetPeers = 8;
+struct RetMaps {
+  CUtensorMap m[kMaxRetPeers];
+  int n;
 };
 
 // A tile load (128 x 64) for the current stage
@@ -549,7 +563,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
-                        const __grid_constant__ CUtensorMap map_x, const Params p) {
+                        const __grid_constant__ CUtensorMap map_x, const Params p,
+                        const __grid_constant__ RetMaps rmaps) {
   using C = Cfg<CG, AUX>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -750,6 +765,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) hnext[q] = ld_nc_v4(aux_rd + q * 32);
         }
+        // scatter epilogue: this lane's output row goes straight back (NVLink store) to
+        // the rank that sent it -- the combine / dispatch-backward then read locally
+        uint4* sc_dst = nullptr;
+        const CUtensorMap* smap = &map_c;   // TMA store target and row of this warp's chunk
+        int srow = row0;
+        bool scatter = false;               // per-row direct stores (non-contiguous chunk)
+        if constexpr (K == 0) {
+          if (p.ret_map) {
+            const long long code = __ldg(p.ret_map + row0 + lane);
+            const long long cf = __shfl_sync(0xffffffffu, code, 0);
+            const long long cl = __shfl_sync(0xffffffffu, code, 31);
+            if (cf >= 0 && cl - cf == 31 && (cf >> 32) == (cl >> 32) && (cf >> 32) < rmaps.n) {
+              smap = &rmaps.m[cf >> 32];
+              srow = (int)(cf & 0xffffffffll);
+            } else {
+              scatter = true;
+              if (code >= 0)
+                sc_dst = reinterpret_cast<uint4*>(p.ret_peers[code >> 32]) +
+                         (code & 0xffffffffll) * (p.N >> 3) + (col0 >> 3);
+            }
+          }
+        }
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols +
@@ -792,6 +829,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int q = 0; q < 4; ++q) hnext[q] = ld_nc_v4(aux_rd + (c + 1) * 128 + q * 32);
             }
           }
+          if (scatter) {
+            if (sc_dst) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) st_v4(sc_dst + c * 4 + q, f32_to_bf16x8(f + 8 * q));
+            }
+            continue;
+          }
           // the store that used buffer b (chunk c-2) must have finished reading smem
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
@@ -818,7 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&map_c, wbuf + b * kEpiBuf, col0 + c * kEpiCols, row0);
+            tma_store_2d(smap, wbuf + b * kEpiBuf, col0 + c * kEpiCols, srow);
             bulk_commit();
           }
         }
@@ -903,7 +947,8 @@ extern "C" int lz_gemm_row_align(void) { return BM * g_cta_group; }
 
 template <int A_MN, int B_MN, int CG, bool AUX>
 static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                        const CUtensorMap& mx, const Params& p, int grid, cudaStream_t s) {
+                        const CUtensorMap& mx, const Params& p, const RetMaps& rm, int grid,
+                        cudaStream_t s) {
   auto kern = grouped_gemm_kernel<A_MN, B_MN, CG, AUX>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -924,35 +969,74 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, p) != cudaSuccess) return lzh::check_launch();
+  if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, p, rm) != cudaSuccess)
+    return lzh::check_launch();
   return lzh::check_launch();
 }
 
 template <int A_MN, int B_MN, bool AUX>
 static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                           const CUtensorMap& mx, const Params& p, long tiles, int sms,
-                           cudaStream_t s) {
+                           const CUtensorMap& mx, const Params& p, const RetMaps& rm, long tiles,
+                           int sms, cudaStream_t s) {
   if (g_cta_group == 2) {
     long units = tiles < sms / 2 ? tiles : sms / 2;
     if (units < 1) units = 1;
-    return launch<A_MN, B_MN, 2, AUX>(ma, mb, mc, mx, p, (int)(2 * units), s);
+    return launch<A_MN, B_MN, 2, AUX>(ma, mb, mc, mx, p, rm, (int)(2 * units), s);
   }
   long grid = tiles < sms ? tiles : sms;
   if (grid < 1) grid = 1;
-  return launch<A_MN, B_MN, 1, AUX>(ma, mb, mc, mx, p, (int)grid, s);
+  return launch<A_MN, B_MN, 1, AUX>(ma, mb, mc, mx, p, rm, (int)grid, s);
 }
 template <int A_MN, int B_MN>
 static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
-                           const CUtensorMap& mx, const Params& p, long tiles, int sms,
-                           cudaStream_t s) {
-  return p.epilogue == LZ_EPI_STORE ? launch_cg<A_MN, B_MN, false>(ma, mb, mc, mx, p, tiles, sms, s)
-                                    : launch_cg<A_MN, B_MN, true>(ma, mb, mc, mx, p, tiles, sms, s);
+                           const CUtensorMap& mx, const Params& p, const RetMaps& rm, long tiles,
+                           int sms, cudaStream_t s) {
+  return p.epilogue == LZ_EPI_STORE
+             ? launch_cg<A_MN, B_MN, false>(ma, mb, mc, mx, p, rm, tiles, sms, s)
+             : launch_cg<A_MN, B_MN, true>(ma, mb, mc, mx, p, rm, tiles, sms, s);
 }
+
+static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void* C, void* aux,
+                                   int G, const int32_t* off, int rows_total, int M, int N,
+                                   int K, int b_major, int epilogue, int num_sms,
+                                   int c_group_rows, int c_row_offset, void* stream,
+                                   const long long* ret_map, const unsigned long long* ret_peers,
+                                   const RetMaps& rm);
 
 extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
                                      int G, const int32_t* off, int rows_total, int M, int N,
                                      int K, int b_major, int epilogue, int num_sms,
                                      int c_group_rows, int c_row_offset, void* stream) {
+  static const RetMaps none{};
+  return grouped_gemm_impl(mode, A, B, C, aux, G, off, rows_total, M, N, K, b_major, epilogue,
+                           num_sms, c_group_rows, c_row_offset, stream, nullptr, nullptr, none);
+}
+
+extern "C" lz_status lz_grouped_gemm_scatter(const void* A, const void* B, void* C, int G,
+                                             const int32_t* off, int rows_total, int N, int K,
+                                             int b_major, int num_sms,
+                                             const long long* ret_map,
+                                             const unsigned long long* ret_peers,
+                                             const unsigned long long* ret_peers_host,
+                                             int n_peers, int ret_rows, void* stream) {
+  if (!ret_map || !ret_peers || n_peers < 0 || ret_rows < 0 || (n_peers > 0 && !ret_peers_host))
+    return LZ_ERR_ARG;
+  RetMaps rm{};
+  rm.n = n_peers <= kMaxRetPeers ? n_peers : 0;   // more ranks: per-row stores only
+  for (int r = 0; r < rm.n; ++r)
+    if (!make_map(&rm.m[r], (void*)ret_peers_host[r], N, ret_rows > 0 ? ret_rows : 1, kEpiCols,
+                  32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return LZ_ERR_CUDA;
+  return grouped_gemm_impl(0, A, B, C, nullptr, G, off, rows_total, 0, N, K, b_major,
+                           LZ_EPI_STORE, num_sms, 0, 0, stream, ret_map, ret_peers, rm);
+}
+
+static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void* C, void* aux,
+                                   int G, const int32_t* off, int rows_total, int M, int N,
+                                   int K, int b_major, int epilogue, int num_sms,
+                                   int c_group_rows, int c_row_offset, void* stream,
+                                   const long long* ret_map, const unsigned long long* ret_peers,
+                                   const RetMaps& rm) {
   if (G < 1 || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
   if (G > kMaxGroups) return LZ_ERR_UNSUPPORTED;
   if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DSWIGLU) return LZ_ERR_ARG;
@@ -975,6 +1059,8 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
   p.aux = (__nv_bfloat16*)aux;
   p.ldc = N;
   p.ldx = N;
+  p.ret_map = ret_map;
+  p.ret_peers = ret_peers;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (sms < 2) sms = 2;
@@ -997,8 +1083,8 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
     if (!make_map(&mx, aux ? aux : C, x_w, rows_total, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     // upper bound of tiles; the kernel reads the exact count from the device offsets
     long tiles = (long)(rows_total / tile_m) * (N / BN);
-    return b_major == LZ_K_MAJOR ? launch_cg<0, 0>(ma, mb, mc, mx, p, tiles, sms, s)
-                                 : launch_cg<0, 1>(ma, mb, mc, mx, p, tiles, sms, s);
+    return b_major == LZ_K_MAJOR ? launch_cg<0, 0>(ma, mb, mc, mx, p, rm, tiles, sms, s)
+                                 : launch_cg<0, 1>(ma, mb, mc, mx, p, rm, tiles, sms, s);
   } else if (mode == 1) {
     if (M <= 0 || M % tile_m) return LZ_ERR_UNSUPPORTED;
     if (c_group_rows != 0 && (c_group_rows < M || c_row_offset < 0 ||
@@ -1010,7 +1096,7 @@ extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, voi
     const uint64_t c_rows = (uint64_t)(G - 1) * p.c_grp_rows + c_row_offset + M;
     if (!make_map(&mc, C, N, c_rows, kEpiCols, 32, sw64)) return LZ_ERR_CUDA;
     long tiles = (long)G * (M / tile_m) * (N / BN);
-    return launch_cg<1, 1>(ma, mb, mc, mc, p, tiles, sms, s);
+    return launch_cg<1, 1>(ma, mb, mc, mc, p, rm, tiles, sms, s);
   }
   return LZ_ERR_ARG;
 }

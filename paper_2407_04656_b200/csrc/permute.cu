@@ -16,7 +16,7 @@ constexpr int kVec = 4;  // uint4 per lane in flight
 
 __device__ __forceinline__ void zero_pad_rows(void* out, int d, int E, const int32_t* recv_m,
                                               const int32_t* recv_off, long item, long n_items,
-                                              int lane) {
+                                              int lane, long long* ret_own = nullptr) {
   // item enumerates (expert, pad row) pairs; pad rows are [off[e]+m[e], off[e+1])
   (void)n_items;
   const int nch = d / 8;
@@ -26,6 +26,7 @@ __device__ __forceinline__ void zero_pad_rows(void* out, int d, int E, const int
     if (item < cnt) {
       uint4* dst = reinterpret_cast<uint4*>(out) + (start + item) * nch;
       for (int c = lane; c < nch; c += 32) st_v4(dst + c, make_uint4(0, 0, 0, 0));
+      if (ret_own && lane == 0) ret_own[start + item] = -1;   // pad row: no return target
       return;
     }
     item -= cnt;
@@ -41,22 +42,32 @@ __device__ __forceinline__ uint4* row_base(uint4* local, const unsigned long lon
   return reinterpret_cast<uint4*>(peers[r]);
 }
 
+// ret_peers (optional): every rank's return map; the owner row receiving assignment
+// p = t*k + s of this rank records (my_rank << 32 | ret_row[p]) -- ret_row = the send
+// slot, so each (owner, expert) segment maps to a contiguous row range here and the
+// owner's GEMM epilogue can TMA-store the expert output straight back into this rank's
+// return buffer.
 __global__ void __launch_bounds__(kRowThreads) pack_kernel(
     const uint4* __restrict__ x, int Tn, int d, int k, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers,
     uint4* __restrict__ out, int E, const int32_t* __restrict__ recv_m,
-    const int32_t* __restrict__ recv_off, long n_pad_items) {
+    const int32_t* __restrict__ recv_off, long n_pad_items,
+    const unsigned long long* __restrict__ ret_peers, long long* __restrict__ ret_own,
+    int my_rank, const int32_t* __restrict__ ret_row) {
   const int lane = threadIdx.x % 32;
   const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
   const long nw = (long)gridDim.x * kRowWarps;
   const int nch = d / 8;
   for (long t = gw; t < Tn + n_pad_items; t += nw) {
     if (t >= Tn) {
-      zero_pad_rows(out, d, E, recv_m, recv_off, t - Tn, n_pad_items, lane);
+      zero_pad_rows(out, d, E, recv_m, recv_off, t - Tn, n_pad_items, lane, ret_own);
       continue;
     }
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
     const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
+    if (ret_peers && lane < k)
+      reinterpret_cast<long long*>(ret_peers[my_rk])[my_row] =
+          ((long long)my_rank << 32) | (long long)__ldg(ret_row + t * k + lane);
     const uint4* src = x + t * nch;
     for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
       uint4 v[kVec];
@@ -123,7 +134,11 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
     const unsigned long long* __restrict__ peers_dy,
     const float* __restrict__ w, int Tn, int d, int k, uint4* __restrict__ dy,
     float* __restrict__ dw, int E, const int32_t* __restrict__ recv_m,
-    const int32_t* __restrict__ recv_off, long n_pad_items) {
+    const int32_t* __restrict__ recv_off, long n_pad_items,
+    const int32_t* __restrict__ yrow) {
+  // yrow (optional): y is this rank's own return buffer and assignment p's expert output
+  // sits at row yrow[p] (written by the owners' scattering GEMM epilogue); dy still goes
+  // to the owner's row
   const int lane = threadIdx.x % 32;
   const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
   const long nw = (long)gridDim.x * kRowWarps;
@@ -134,8 +149,9 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
       continue;
     }
     const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const int my_yrow = (yrow && lane < k) ? __ldg(yrow + t * k + lane) : 0;
     const float my_w = lane < k ? __ldg(w + t * k + lane) : 0.f;
-    const int my_rk = (peers_y && lane < k) ? __ldg(prank + t * k + lane) : 0;
+    const int my_rk = ((peers_y || peers_dy) && lane < k) ? __ldg(prank + t * k + lane) : 0;
     float dot[LZ_MAX_TOPK];
 #pragma unroll
     for (int s = 0; s < LZ_MAX_TOPK; ++s) dot[s] = 0.f;
@@ -149,7 +165,8 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
         if (s >= k) break;
         const long r = __shfl_sync(0xffffffffu, my_row, s);
         const float ws = __shfl_sync(0xffffffffu, my_w, s);
-        const uint4* ys = row_base(const_cast<uint4*>(y), peers_y, my_rk, s) + r * nch;
+        const uint4* ys = yrow ? y + (long)__shfl_sync(0xffffffffu, my_yrow, s) * nch
+                               : row_base(const_cast<uint4*>(y), peers_y, my_rk, s) + r * nch;
         uint4* dys = row_base(dy, peers_dy, my_rk, s) + r * nch;
         uint4 v[kVec];
 #pragma unroll
@@ -676,14 +693,18 @@ static constexpr int kPadAlign = 256;  // >= the largest GEMM row alignment (lz_
 
 static lz_status pack_impl(const void* x, int Tn, int d, int k, const int32_t* row,
                            const int32_t* prank, const unsigned long long* peers, void* out, int E,
-                           const int32_t* recv_m, const int32_t* recv_off, void* stream) {
+                           const int32_t* recv_m, const int32_t* recv_off, void* stream,
+                           const unsigned long long* ret_peers = nullptr,
+                           long long* ret_own = nullptr, int my_rank = 0,
+                           const int32_t* ret_row = nullptr) {
   if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
   if (Tn > 0 && (!x || !row || !out)) return LZ_ERR_ARG;
   if (E > 0 && (!recv_m || !recv_off || !out)) return LZ_ERR_ARG;
   const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
   if (Tn + npad == 0) return LZ_OK;
   pack_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, Tn, d, k, row, prank, peers, (uint4*)out, E, recv_m, recv_off, npad);
+      (const uint4*)x, Tn, d, k, row, prank, peers, (uint4*)out, E, recv_m, recv_off, npad,
+      ret_peers, ret_own, my_rank, ret_row);
   return lzh::check_launch();
 }
 
@@ -699,6 +720,18 @@ extern "C" lz_status lz_pack_p2p(const void* x, int Tn, int d, int k, const int3
                                  const int32_t* recv_off, void* stream) {
   if (!peers || !dest_rank) return LZ_ERR_ARG;
   return pack_impl(x, Tn, d, k, dest_row, dest_rank, peers, own, E, recv_m, recv_off, stream);
+}
+
+extern "C" lz_status lz_pack_p2p_ret(const void* x, int Tn, int d, int k,
+                                     const int32_t* dest_rank, const int32_t* dest_row,
+                                     const unsigned long long* peers, void* own, int E,
+                                     const int32_t* recv_m, const int32_t* recv_off,
+                                     const unsigned long long* ret_peers, long long* ret_own,
+                                     int my_rank, const int32_t* ret_row, void* stream) {
+  if (!peers || !dest_rank || !ret_peers || !ret_own || my_rank < 0 || (Tn > 0 && !ret_row))
+    return LZ_ERR_ARG;
+  return pack_impl(x, Tn, d, k, dest_row, dest_rank, peers, own, E, recv_m, recv_off, stream,
+                   ret_peers, ret_own, my_rank, ret_row);
 }
 
 static lz_status combine_impl(const void* y, const int32_t* row, const int32_t* prank,
@@ -728,7 +761,8 @@ static lz_status combine_bwd_impl(const void* dout, const void* y, const int32_t
                                   const int32_t* prank, const unsigned long long* peers_y,
                                   const unsigned long long* peers_dy, const float* w, int Tn,
                                   int d, int k, void* dy, float* dw, int E,
-                                  const int32_t* recv_m, const int32_t* recv_off, void* stream) {
+                                  const int32_t* recv_m, const int32_t* recv_off, void* stream,
+                                  const int32_t* yrow = nullptr) {
   if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK || E < 0) return LZ_ERR_ARG;
   if (Tn > 0 && (!dout || (!y && !peers_y) || !row || !w || (!dy && !peers_dy) || !dw))
     return LZ_ERR_ARG;
@@ -737,7 +771,7 @@ static lz_status combine_bwd_impl(const void* dout, const void* y, const int32_t
   if (Tn + npad == 0) return LZ_OK;
   combine_bwd_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
       (const uint4*)dout, (const uint4*)y, row, prank, peers_y, peers_dy, w, Tn, d, k, (uint4*)dy,
-      dw, E, recv_m, recv_off, npad);
+      dw, E, recv_m, recv_off, npad, yrow);
   return lzh::check_launch();
 }
 
@@ -758,6 +792,18 @@ extern "C" lz_status lz_combine_bwd_p2p(const void* dout, const unsigned long lo
   if (!peers_y || !peers_dy || !dest_rank) return LZ_ERR_ARG;
   return combine_bwd_impl(dout, nullptr, dest_row, dest_rank, peers_y, peers_dy, w, Tn, d, k,
                           own_dy, dw, E, recv_m, recv_off, stream);
+}
+
+extern "C" lz_status lz_combine_bwd_p2p_ret(const void* dout, const void* y_ret,
+                                            const int32_t* y_row,
+                                            const unsigned long long* peers_dy,
+                                            const int32_t* dest_rank, const int32_t* dest_row,
+                                            const float* w, int Tn, int d, int k, float* dw,
+                                            void* own_dy, int E, const int32_t* recv_m,
+                                            const int32_t* recv_off, void* stream) {
+  if (!y_ret || !peers_dy || !dest_rank || (Tn > 0 && !y_row)) return LZ_ERR_ARG;
+  return combine_bwd_impl(dout, y_ret, dest_row, dest_rank, nullptr, peers_dy, w, Tn, d, k,
+                          own_dy, dw, E, recv_m, recv_off, stream, y_row);
 }
 
 static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const int32_t* prank,

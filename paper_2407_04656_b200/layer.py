@@ -105,6 +105,9 @@ class MoELayer(torch.nn.Module):
         self._fwd_version = 0
         self.stage_events: list | None = None
         self.load_window = None   # rebalance.LoadWindow, attached by rebalance.Rebalancer
+        # P2P exchange: return expert outputs from the GEMM epilogues (default) instead of
+        # reading them back over NVLink in the combine / dispatch backward
+        self.scatter = os.environ.get("LZ_P2P_SCATTER", "1") != "0"
         # SMs the backward GEMMs leave to NCCL while the expert-gradient all-reduce runs
         self.overlap_reserve = int(os.environ.get("LZ_OVERLAP_SMS", "16"))
         self.set_plan(replicas)
@@ -245,13 +248,19 @@ class _MoEFunction(torch.autograd.Function):
             Y = torch.empty((cap, d), dtype=torch.bfloat16, device=x.device)
             ops.pack(x, plan.dest_row, k, X, plan.recv_m, plan.recv_off)
         elif mode == "p2p":
-            # fused dispatch: rows go straight into the destination's symmetric buffer
+            # fused dispatch: rows go straight into the destination's symmetric buffer, and
+            # the owner learns where each row came from (return map for the scatter GEMMs)
             sym = layer.symmetric(Tn)
             layer._fwd_version += 1
             cap = sym.rows
             X, Y = sym.buf(0), sym.buf(1)
-            ops.pack_p2p(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X, plan.recv_m,
-                         plan.recv_off)
+            if layer.scatter:
+                ops.pack_p2p_ret(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X,
+                                 plan.recv_m, plan.recv_off, sym.ret_ptrs, sym.ret, rank,
+                                 plan.slot)
+            else:
+                ops.pack_p2p(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X, plan.recv_m,
+                             plan.recv_off)
             sym.barrier()
         else:
             # NCCL exchange: one D2H of the counts (+ error flag) per layer forward
@@ -280,14 +289,26 @@ class _MoEFunction(torch.autograd.Function):
         swi = layer.activation == "swiglu"
         H = torch.empty((cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16, device=x.device)
         A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
+        scatter = mode == "p2p" and layer.scatter
         if G > 0:
             ops.grouped_gemm_rows(X, w1, off, A, aux=H,
                                   epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
-            ops.grouped_gemm_rows(A, w2, off, Y)
+            if scatter:
+                # GEMM + combine all-to-all in one kernel: the epilogue stores every output
+                # row into its source rank's return buffer (row = source assignment)
+                ops.grouped_gemm_scatter(A, w2, off, Y, sym.ret, sym.peers(1), sym.peers_host(1),
+                                         sym.rows)
+            else:
+                ops.grouped_gemm_rows(A, w2, off, Y)
         _mark(layer, "ffn_fwd")
         if mode == "local":
             out = ops.combine(Y, plan.dest_row, w, k)
             ret, row = Y, plan.dest_row
+        elif scatter:
+            sym.barrier()
+            row = plan.slot                     # rows came back to their send slots
+            out = ops.combine(Y, row, w, k)     # local reads only
+            ret = Y
         elif mode == "p2p":
             sym.barrier()
             out = ops.combine_p2p(sym.peers(1), plan.dest_rank, plan.dest_row, w, k, d)
@@ -330,8 +351,12 @@ class _MoEFunction(torch.autograd.Function):
                                    "run backward before the next forward")
             sym = layer.symmetric(Tn)
             dY, dX = sym.buf(2), sym.buf(3)
-            dw = ops.combine_bwd_p2p(dout, sym.peers(1), sym.peers(2), plan.dest_rank,
-                                     plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
+            if layer.scatter:
+                dw = ops.combine_bwd_p2p_ret(dout, ret, row, sym.peers(2), plan.dest_rank,
+                                             plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
+            else:
+                dw = ops.combine_bwd_p2p(dout, sym.peers(1), sym.peers(2), plan.dest_rank,
+                                         plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
             sym.barrier()
         else:
             send_sizes, recv_counts, max_seg = sizes
@@ -366,11 +391,21 @@ class _MoEFunction(torch.autograd.Function):
             ops.grouped_gemm_wgrad(dH, X, off, dW1, num_sms=ov)
         if N > 1:
             works += layer.replica_groups.allreduce_async([dW1], layer.local_ids)
+        scatter = mode == "p2p" and layer.scatter
         if G > 0:
-            # dX = dH . W1 (W1_e [d_ff, d] read MN-major)
-            ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR, num_sms=ov)
+            # dX = dH . W1 (W1_e [d_ff, d] read MN-major); scatter: rows go back to their
+            # source ranks' return buffers (GEMM + dispatch-backward all-to-all fused)
+            if scatter:
+                ops.grouped_gemm_scatter(dH, w1, off, dX, sym.ret, sym.peers(3),
+                                         sym.peers_host(3), sym.rows, b_major=_lib.LZ_MN_MAJOR,
+                                         num_sms=ov)
+            else:
+                ops.grouped_gemm_rows(dH, w1, off, dX, b_major=_lib.LZ_MN_MAJOR, num_sms=ov)
         _mark(layer, "ffn_bwd")
         if mode == "local":
+            dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
+        elif scatter:
+            sym.barrier()
             dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
         elif mode == "p2p":
             sym.barrier()

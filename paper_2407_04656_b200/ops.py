@@ -138,14 +138,14 @@ def router_wgrad(dlogits, x, with_bias: bool = True):
 GEMM_EVENTS: list | None = None
 
 
-def _gemm(*args):
+def _gemm(*args, fn: str = "lz_grouped_gemm"):
     if GEMM_EVENTS is None:
-        _lib.call("lz_grouped_gemm", *args)
+        _lib.call(fn, *args)
         return
     a = torch.cuda.Event(enable_timing=True)
     b = torch.cuda.Event(enable_timing=True)
     a.record()
-    _lib.call("lz_grouped_gemm", *args)
+    _lib.call(fn, *args)
     b.record()
     GEMM_EVENTS.append((a, b))
 
@@ -177,6 +177,25 @@ def aux_blocked(rows_major: torch.Tensor) -> torch.Tensor:
     """Inverse of :func:`aux_rows`."""
     R, N = rows_major.shape
     return rows_major.reshape(R // 32, 32, N // 32, 4, 8).permute(0, 2, 3, 1, 4).reshape(R, N)
+
+
+def grouped_gemm_scatter(A, B, off, C, ret_map, ret_peers, ret_peers_host, ret_rows: int, *,
+                         b_major=_lib.LZ_K_MAJOR, num_sms: int = 0):
+    """Mode-0 store GEMM whose output row r goes to row (ret_map[r] & 0xffffffff) of the
+    return buffer of rank ret_map[r] >> 32 (TMA stores for contiguous 32-row chunks, per-row
+    stores otherwise; NVLink for remote ranks); -1 = pad.  ret_peers: device int64 table of
+    the buffers, ret_peers_host: the same addresses as Python ints, ret_rows: their rows.
+    C ([rows, N], not written) only sizes the launch."""
+    import ctypes
+    _cuda(A, B, off, C, ret_map, ret_peers)
+    rows, K = A.shape
+    G = off.numel() - 1
+    N = B.shape[1] if b_major == _lib.LZ_K_MAJOR else B.shape[2]
+    host = (ctypes.c_ulonglong * max(1, len(ret_peers_host)))(*ret_peers_host)
+    _gemm(ptr(A), ptr(B), ptr(C), G, ptr(off), rows, N, K, b_major, num_sms, ptr(ret_map),
+          ptr(ret_peers), ctypes.cast(host, ctypes.c_void_p), len(ret_peers_host), int(ret_rows),
+          _s(), fn="lz_grouped_gemm_scatter")
+    return C
 
 
 def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0, c_group_rows: int = 0,
@@ -231,6 +250,27 @@ def dispatch_bwd_p2p(peers_dxe, dest_rank, dest_row, probs, idx, dw, wg, renorm:
     _lib.call("lz_dispatch_bwd_p2p", ptr(peers_dxe), ptr(dest_rank), ptr(dest_row), Tn, d, k,
               ptr(probs), ptr(idx), ptr(dw), ptr(wgT), E, int(renorm), ptr(dx), ptr(dlog), _s())
     return dx, dlog
+
+
+def pack_p2p_ret(x, dest_rank, dest_row, k: int, peers, own, recv_m, recv_off, ret_peers,
+                 ret_own, my_rank: int, ret_row):
+    """pack_p2p + the owners' return map (rank << 32 | ret_row[assignment]) for the scatter
+    GEMM (ret_row = the plan's send slot)."""
+    Tn, d = x.shape
+    _lib.call("lz_pack_p2p_ret", ptr(x), Tn, d, k, ptr(dest_rank), ptr(dest_row), ptr(peers),
+              ptr(own), recv_m.numel(), ptr(recv_m), ptr(recv_off), ptr(ret_peers),
+              ptr(ret_own), int(my_rank), ptr(ret_row), _s())
+
+
+def combine_bwd_p2p_ret(dout, y_ret, y_row, peers_dy, dest_rank, dest_row, w, k: int, own_dy,
+                        recv_m, recv_off):
+    """combine backward with y read from this rank's own return buffer at rows y_row."""
+    Tn, d = dout.shape
+    dw = torch.empty((Tn, k), dtype=torch.float32, device=dout.device)
+    _lib.call("lz_combine_bwd_p2p_ret", ptr(dout), ptr(y_ret), ptr(y_row), ptr(peers_dy),
+              ptr(dest_rank), ptr(dest_row), ptr(w), Tn, d, k, ptr(dw), ptr(own_dy),
+              recv_m.numel(), ptr(recv_m), ptr(recv_off), _s())
+    return dw
 
 
 def set_gemm_direct_epilogue(on: int) -> int:

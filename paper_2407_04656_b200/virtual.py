@@ -24,7 +24,7 @@ class VirtualEP:
     def __init__(self, d_model: int, d_ff: int, n_experts: int, top_k: int, replicas,
                  tokens_per_rank: int, *, seed: int = 0, init_std: float = 0.02,
                  router_bias=None, router_std: float | None = None, device=None,
-                 activation: str = "gelu"):
+                 activation: str = "gelu", scatter: bool = False):
         self.d, self.d_ff, self.E, self.k = d_model, d_ff, n_experts, top_k
         self.R = [list(r) for r in replicas]
         self.N = len(self.R[0])
@@ -63,6 +63,16 @@ class VirtualEP:
         self.Y = torch.empty_like(self.X)
         self._none = torch.empty(0, dtype=torch.int32, device=dev)
         self.last_plans = None
+        # scatter mode (the multi-GPU default): the second GEMM's epilogue writes every
+        # output row straight back to its source rank's return buffer (row = assignment),
+        # through the owner-side return map the dispatch records
+        self.scatter = scatter
+        if scatter:
+            P = tokens_per_rank * top_k
+            self.RET = torch.empty(self.cap, dtype=torch.int64, device=dev)
+            self.YR = torch.empty((self.N, P, d_model), dtype=torch.bfloat16, device=dev)
+            self.ret_host = [self.YR[r].data_ptr() for r in range(self.N)]
+            self.peers_ret = torch.tensor(self.ret_host, dtype=torch.int64, device=dev)
 
     @torch.no_grad()
     def forward(self, xs):
@@ -79,16 +89,27 @@ class VirtualEP:
         peers_x = base * row_b + self.X.data_ptr()
         peers_y = base * row_b + self.Y.data_ptr()
         off = (offs + base[:, None]).view(-1).index_select(0, self.flat).to(torch.int32)
+        if self.scatter:
+            ret_peers = base * 8 + self.RET.data_ptr()
+            self.RET.fill_(-1)   # pad rows of every region
         for r in range(N):   # every rank scatters its rows into the owners' regions
             # forward only: pad rows are never read back, so they are not zeroed (E = 0)
-            ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
-                         self._none, self._none)
+            if self.scatter:
+                ops.pack_p2p_ret(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
+                                 self._none, self._none, ret_peers, self.RET, r, plans[r].slot)
+            else:
+                ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
+                             self._none, self._none)
         swi = self.activation == "swiglu"
         H = torch.empty((self.cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16,
                         device=self.device)
         A = torch.empty((self.cap, d_ff), dtype=torch.bfloat16, device=self.device)
         ops.grouped_gemm_rows(self.X, self.w1, off, A, aux=H,
                               epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
+        if self.scatter:
+            ops.grouped_gemm_scatter(A, self.w2, off, self.Y, self.RET, self.peers_ret,
+                                     self.ret_host, self.YR.shape[1])
+            return [ops.combine(self.YR[r], plans[r].slot, gates[r][1], k) for r in range(N)]
         ops.grouped_gemm_rows(A, self.w2, off, self.Y)
         return [ops.combine_p2p(peers_y, plans[r].dest_rank, plans[r].dest_row, gates[r][1],
                                 k, d) for r in range(N)]

@@ -12,7 +12,7 @@ from oracle import dispatch_ref
 pytestmark = pytest.mark.gpu
 
 
-def _setup(N, E, k, d, dff, Tn, act, zipf, seed=3):
+def _setup(N, E, k, d, dff, Tn, act, zipf, seed=3, scatter=False):
     from paper_2407_04656_b200.layer import MoELayer, zipf_router_bias, default_slots
     from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix
     from paper_2407_04656_b200.virtual import VirtualEP
@@ -20,18 +20,26 @@ def _setup(N, E, k, d, dff, Tn, act, zipf, seed=3):
     loads = [int(1000 / (e + 1) ** (zipf or 0.0)) + 1 for e in range(E)]
     plan = plan_for_loads(loads, N, default_slots(E, N), fault_threshold=min(2, N))
     R = replica_matrix(plan)
-    vep = VirtualEP(d, dff, E, k, R, Tn, seed=seed, router_bias=bias, activation=act)
+    vep = VirtualEP(d, dff, E, k, R, Tn, seed=seed, router_bias=bias, activation=act,
+                    scatter=scatter)
     ref = MoELayer(d, dff, E, k, seed=seed, router_bias=bias, activation=act)
     torch.manual_seed(seed)
     xs = [torch.randn(Tn, d, device="cuda").bfloat16() for _ in range(N)]
     return vep, ref, xs, R
 
 
-@pytest.mark.parametrize("N,E,k,act,zipf", [(4, 8, 2, "gelu", 1.2), (8, 16, 2, "gelu", 0.8),
-                                             (8, 8, 1, "swiglu", 1.5), (3, 8, 2, "gelu", 0.0)])
-def test_virtual_ranks_match_single_rank(N, E, k, act, zipf):
+@pytest.mark.parametrize("N,E,k,act,zipf,scatter", [(4, 8, 2, "gelu", 1.2, False),
+                                                     (8, 16, 2, "gelu", 0.8, False),
+                                                     (8, 8, 1, "swiglu", 1.5, False),
+                                                     (3, 8, 2, "gelu", 0.0, False),
+                                                     (4, 8, 2, "gelu", 1.2, True),
+                                                     (8, 16, 2, "swiglu", 0.8, True),
+                                                     (3, 8, 1, "gelu", 0.0, True)])
+def test_virtual_ranks_match_single_rank(N, E, k, act, zipf, scatter):
+    """scatter=True: the second GEMM's epilogue returns rows to their source rank (the
+    multi-GPU default) -- same bits as the gathered combine."""
     d, dff, Tn = 512, 1024, 1024
-    vep, ref, xs, R = _setup(N, E, k, d, dff, Tn, act, zipf)
+    vep, ref, xs, R = _setup(N, E, k, d, dff, Tn, act, zipf, scatter=scatter)
     with torch.no_grad():
         outs = vep(xs)
         torch.cuda.synchronize()
