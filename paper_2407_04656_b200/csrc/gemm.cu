@@ -316,10 +316,8 @@ struct Params {
   int M, N, K;      // mode 0: N, K used; mode 1: M, N
   const int32_t* off;
   int epilogue;
-  int direct;              // 1: epilogue stores straight from registers (no smem staging)
-  __nv_bfloat16* C;        // direct epilogue: output base and row stride (elements)
+  __nv_bfloat16* C;
   __nv_bfloat16* aux;
-  long ldc, ldx;
   // scatter epilogue (store variant, mode 0): output row r goes to rank (ret_map[r] >> 32)
   // at row (ret_map[r] & 0xffffffff) of its buffer ret_peers[rank] (row length N); -1 = pad
   const long long* ret_map;
@@ -932,11 +930,12 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 }
 
 static int g_cta_group = 2;  // default: CTA-pair kernel
-static int g_direct_epi = 0;  // 1: register -> global epilogue, 0: smem staging + TMA store
 
+// ABI compatibility: the register -> global epilogue variants were measured 1.6-2x slower
+// than smem staging + TMA stores and removed; the switch is a no-op.
 extern "C" int lz_gemm_set_direct_epilogue(int on) {
-  if (on >= 0 && on <= 2) g_direct_epi = on;
-  return g_direct_epi;
+  (void)on;
+  return 0;
 }
 
 extern "C" int lz_gemm_set_cta_group(int cg) {
@@ -1054,11 +1053,8 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
   p.epilogue = epilogue;
   p.c_grp_rows = c_group_rows > 0 ? c_group_rows : M;
   p.c_row_off = c_row_offset;
-  p.direct = 0;  // register->global epilogue variants were measured 1.6-2x slower; removed
   p.C = (__nv_bfloat16*)C;
   p.aux = (__nv_bfloat16*)aux;
-  p.ldc = N;
-  p.ldx = N;
   p.ret_map = ret_map;
   p.ret_peers = ret_peers;
   cudaStream_t s = (cudaStream_t)stream;

@@ -279,5 +279,3 @@ def set_gemm_direct_epilogue(on: int) -> int:
 
 if "LZ_GEMM_CTA" in __import__("os").environ:  # A/B switch for the GEMM variant
     set_gemm_cta_group(int(__import__("os").environ["LZ_GEMM_CTA"]))
-if "LZ_GEMM_DIRECT" in __import__("os").environ:  # A/B switch for the epilogue store path
-    set_gemm_direct_epilogue(int(__import__("os").environ["LZ_GEMM_DIRECT"]))

@@ -102,3 +102,53 @@ def test_layer_replan_without_recompile():
         layer.set_plan([[1 + (e % 3)] for e in range(E)])
         b = layer(x)
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("act", ["gelu", "swiglu"])
+def test_graphed_step_matches_eager(act):
+    """GraphedStep (whole fwd+bwd captured in one CUDA graph, replayed) produces the
+    same output checksum and bit-identical gradients as the eager step."""
+    from paper_2407_04656_b200.graphs import GraphedStep
+    torch.manual_seed(3)
+    E, d, dff, k, Tn = 8, 512, 1024, 2, 2048
+    layer = MoELayer(d, dff, E, k, seed=9, router_bias=zipf_router_bias(E, 1.2),
+                     activation=act)
+    layer.set_plan([[1 + (e % 3)] for e in range(E)])
+    x = torch.randn(Tn, d, device="cuda").bfloat16()
+    dout = (torch.randn(Tn, d, device="cuda") * 0.1).bfloat16()
+    layer.zero_grad(set_to_none=True)
+    out = layer(x)
+    out.backward(dout)
+    ref_sum = out.detach().float().sum()
+    ref = {n: p.grad.clone() for n, p in layer.named_parameters()}
+    del out
+    gs = GraphedStep(layer, Tn, nbuf=2)
+    for b in range(2):
+        gs.x[b].copy_(x)
+        gs.dout[b].copy_(dout)
+    for b in (0, 1, 0):
+        res = gs.replay(b)
+        torch.cuda.synchronize()
+        assert torch.allclose(res.cpu(), ref_sum.cpu().view(1), rtol=1e-6)
+        for n, p in layer.named_parameters():
+            assert torch.equal(p.grad, ref[n]), n
+
+
+def test_layer_empty_experts_and_top1():
+    """Experts that receive no token (zero-row groups), k = 1 and a 64-expert router."""
+    torch.manual_seed(4)
+    E, d, dff, k, Tn = 64, 256, 512, 1, 300
+    bias = torch.full((E,), -30.0)
+    bias[:3] = 0.0   # only experts 0..2 can win: 61 empty groups
+    layer = MoELayer(d, dff, E, k, seed=2, router_bias=bias)
+    x = torch.randn(Tn, d, device="cuda").bfloat16().requires_grad_(True)
+    out = layer(x)
+    out.backward(torch.ones_like(out))
+    torch.cuda.synchronize()
+    layer.check()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(x.grad.float()).all()
+    used = set(layer.last_plan.D.sum(dim=(0, 2)).nonzero().view(-1).tolist())
+    assert used <= {0, 1, 2}
+    for p, e in enumerate(layer.local_ids):
+        if e not in used:
+            assert float(layer.w1.grad[p].float().abs().max()) == 0.0
