@@ -276,6 +276,24 @@ int lz_gemm_row_align(void);
 lz_status lz_recovery_count(const unsigned long long* holders, int E, int n_nodes, int k_failed,
                             unsigned long long* good, void* stream);
 
+/* ------------------------------------------------- arrival flags (multi-GPU exchange) */
+
+/* ++*epoch on the stream (one per layer step; every rank bumps its own counter). */
+lz_status lz_epoch_bump(int* epoch, void* stream);
+/* After this rank's dispatch kernel on the stream: flag_peers[j][my_rank] = *epoch for every
+ * rank j < n (system-scope release after a system fence).  flag_peers: device table of
+ * the n ranks' flag arrays (symmetric int32 [n]). */
+lz_status lz_signal_peers(const unsigned long long* flag_peers, int n, int my_rank,
+                          const int* epoch, void* stream);
+/* Arrival-ordered mode-0 grouped GEMM (the first expert GEMM of each direction on N > 1):
+ * as lz_grouped_gemm(mode 0), but the tiles lying entirely inside self_rows[2g] ..
+ * self_rows[2g+1] (the rows this rank dispatched to itself) run first, and the producer
+ * acquires flags[0..n_flags) >= *epoch before the first tile with other ranks' rows. */
+lz_status lz_grouped_gemm_arrival(const void* A, const void* B, void* C, void* aux, int G,
+                                  const int32_t* off, int rows_total, int N, int K, int b_major,
+                                  int epilogue, int num_sms, const int32_t* self_rows,
+                                  const int* flags, int n_flags, const int* epoch, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,10 @@ _SIGS = {
                         _vp],
     "lz_combine_bwd_p2p_ret": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp,
                                _vp, _vp],
+    "lz_epoch_bump": [_vp, _vp],
+    "lz_signal_peers": [_vp, _i, _i, _vp, _vp],
+    "lz_grouped_gemm_arrival": [_vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _i,
+                                _vp, _vp],
     "lz_grouped_gemm_scatter": [_vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _i,
                                 _i, _vp],
     "lz_gate_topk": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
@@ -102,7 +106,8 @@ _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
             "lz_router_wgrad": 2, "lz_grouped_gemm": 1, "lz_pack_p2p": 1, "lz_combine_p2p": 1,
             "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1, "lz_load_record": 1,
             "lz_recovery_count": 1, "lz_pack_p2p_ret": 1, "lz_combine_bwd_p2p_ret": 1,
-            "lz_grouped_gemm_scatter": 1}
+            "lz_grouped_gemm_scatter": 1, "lz_epoch_bump": 1, "lz_signal_peers": 1,
+            "lz_grouped_gemm_arrival": 1}
 launch_count = 0
 
 

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT = os.path.join(PKG, "liblz.so")
 BUILD = os.path.join(ROOT, "build", "lz")
-SOURCES = ["api.cu", "plan.cu", "gate.cu", "permute.cu", "gemm.cu", "reliability.cu"]
+SOURCES = ["api.cu", "plan.cu", "gate.cu", "permute.cu", "gemm.cu", "reliability.cu", "signal.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]

@@ -74,6 +74,17 @@ class SymmetricRows:
         self.ret_ptrs = torch.tensor(
             [self.hr.get_remote_tensor(r, (rows,), torch.int64).data_ptr() for r in range(n)],
             dtype=torch.int64, device=device)
+        # arrival flags [2 (dispatch, combine-backward), n senders] + this rank's step epoch
+        self.n = n
+        self.flags = symm.empty((2, n), dtype=torch.int32, device=device)
+        self.flags.zero_()
+        self.hf = symm.rendezvous(self.flags, group)
+        fb = [self.hf.get_remote_tensor(r, (2, n), torch.int32).data_ptr() for r in range(n)]
+        self.flag_peers = torch.tensor([[b + i * n * 4 for b in fb] for i in range(2)],
+                                       dtype=torch.int64, device=device)
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)
+        self.hf.barrier(channel=0)   # every rank's flags are zero before anyone signals
 
     def buf(self, i: int) -> torch.Tensor:
         return self.t[i]

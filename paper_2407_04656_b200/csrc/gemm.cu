@@ -8,7 +8,7 @@
 // (2 x 256 columns) so the epilogue of tile i overlaps the main loop of tile i+1.
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one lane issues tcgen05.mma)
-//   warps 2..5  epilogue: tcgen05.ld 32x32b -> fused activation -> bf16 -> global
+//   warps 2..9  epilogue: tcgen05.ld 32x32b -> fused activation -> bf16 -> smem -> TMA store
 // The reference has no FFN code; semantics follow PAPER.md:143
 // (one weight copy per (expert, rank); R[e][j] > 1 only scales capacity).
 #include <cuda.h>  // CUtensorMap (header only; the encoder is fetched at run time)
@@ -322,6 +322,13 @@ struct Params {
   // at row (ret_map[r] & 0xffffffff) of its buffer ret_peers[rank] (row length N); -1 = pad
   const long long* ret_map;
   const unsigned long long* ret_peers;
+  // arrival-ordered row GEMM (mode 0, multi-GPU): self_rows[2g], [2g+1] = rows of group g
+  // this rank sent to itself; tiles fully inside them run first, every other tile waits
+  // until flags[0..n_flags) (written by the senders after their dispatch) reach *epoch
+  const int32_t* self_rows;
+  const int* flags;
+  int n_flags;
+  const int* epoch;
 };
 
 // Per-rank tensor maps of the scatter GEMM's return buffers ([rows, N] bf16 each): a
@@ -359,28 +366,71 @@ __device__ __forceinline__ void load_b(const CUtensorMap* map, uint8_t* dst, uin
 
 struct TileInfo {
   int g, mb, nb, nk;
+  bool remote;   // may contain rows dispatched by other ranks (arrival-ordered GEMM)
 };
 
 template <int CG>
 __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
                                                 const int32_t* s_off, const int32_t* s_perm,
-                                                int tile) {
-  // (tiles are TileM x BN; mb counts TileM blocks).  Tiles are numbered over the groups
-  // in s_perm order: binary search the position i with s_pref[i] <= tile < s_pref[i+1]
+                                                int total0, int tile) {
+  // (tiles are TileM x BN; mb counts TileM blocks).
+  // mode 1: tiles numbered over the groups in s_perm order (descending K).
+  // mode 0: class-0 tiles (fully inside a group's self rows, count s_perm[g] >> 16 m-blocks
+  //         from m-block s_perm[g] & 0xffff) come first, then the class-1 rest in group
+  //         order (prefix s_pref); without self rows class 0 is empty.
+  const int nbn = p.N / BN;
+  TileInfo t;
+  t.remote = false;
+  if (p.mode == 0 && tile < total0) {
+    int acc = 0, g = 0;
+    for (; g < p.G - 1; ++g) {
+      const int n0 = (s_perm[g] >> 16) * nbn;
+      if (tile < acc + n0) break;
+      acc += n0;
+    }
+    const int local = tile - acc;
+    t.g = g;
+    t.mb = (s_perm[g] & 0xffff) + local / nbn;
+    t.nb = local % nbn;
+    t.nk = p.K / BK;
+    return t;
+  }
+  const int t1 = p.mode == 0 ? tile - total0 : tile;
   int lo = 0, hi = p.G - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (s_pref[mid] <= tile) lo = mid;
+    if (s_pref[mid] <= t1) lo = mid;
     else hi = mid - 1;
   }
-  TileInfo t;
-  t.g = s_perm[lo];
-  const int local = tile - s_pref[lo];
-  const int nbn = p.N / BN;
-  t.mb = local / nbn;
+  const int local = t1 - s_pref[lo];
   t.nb = local % nbn;
-  t.nk = (p.mode == 0) ? p.K / BK : (s_off[t.g + 1] - s_off[t.g]) / BK;
+  if (p.mode == 0) {
+    t.g = lo;
+    const int mbl = local / nbn, c0 = s_perm[lo] >> 16, mlo = s_perm[lo] & 0xffff;
+    t.mb = mbl < mlo ? mbl : mbl + c0;
+    t.nk = p.K / BK;
+    t.remote = p.self_rows != nullptr;
+  } else {
+    t.g = s_perm[lo];
+    t.mb = local / nbn;
+    t.nk = (s_off[t.g + 1] - s_off[t.g]) / BK;
+  }
   return t;
+}
+
+// Producer side of the arrival-ordered GEMM: wait until every sender has signalled this
+// step's dispatch into our receive buffer (release stores by lz_signal_peers), then make
+// the remote rows visible to the TMA (async proxy).
+__device__ __forceinline__ void wait_arrivals(const Params& p) {
+  int want;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(want) : "l"(p.epoch) : "memory");
+  for (int i = 0; i < p.n_flags; ++i) {
+    int v;
+    do {
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p.flags + i) : "memory");
+    } while (v - want < 0);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // Private "epilogue-native" layout of the aux streams (GELU: gelu'(h); SwiGLU: S | Q),
@@ -573,6 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
   uint32_t* s_tmem = (uint32_t*)(tempty_bar + 2);
+  int32_t* s_total0 = (int32_t*)(s_tmem + 1);   // class-0 tile count (mode 0)
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
@@ -588,28 +639,44 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int g = threadIdx.x; g <= p.G; g += blockDim.x) s_off[g] = p.off[g];
   __syncthreads();
   for (int g = threadIdx.x; g < p.G; g += blockDim.x) {
-    int rank = g;
     if (p.mode == 1) {
       const int kg = s_off[g + 1] - s_off[g];
-      rank = 0;
+      int rank = 0;
       for (int h = 0; h < p.G; ++h) {
         const int kh = s_off[h + 1] - s_off[h];
         rank += (kh > kg) || (kh == kg && h < g);
       }
+      s_perm[rank] = g;
+    } else {
+      // self-row m-block window of group g: (count << 16) | first m-block
+      int c0 = 0, mlo = 0;
+      if (p.self_rows) {
+        const int base = s_off[g];
+        const int lo = p.self_rows[2 * g] - base, hi = p.self_rows[2 * g + 1] - base;
+        mlo = (lo + C::kTileM - 1) / C::kTileM;
+        const int mhi = hi / C::kTileM;
+        c0 = mhi > mlo ? mhi - mlo : 0;
+        if (c0 == 0) mlo = 0;
+      }
+      s_perm[g] = (c0 << 16) | mlo;
     }
-    s_perm[rank] = g;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int acc = 0;
+    int acc = 0, acc0 = 0;
     const int nbn = p.N / BN;
     for (int i = 0; i < p.G; ++i) {
-      const int g = s_perm[i];
       s_pref[i] = acc;
-      acc += (p.mode == 0) ? ((s_off[g + 1] - s_off[g]) / C::kTileM) * nbn
-                           : (p.M / C::kTileM) * nbn;
+      if (p.mode == 0) {
+        const int c0 = s_perm[i] >> 16;
+        acc += ((s_off[i + 1] - s_off[i]) / C::kTileM - c0) * nbn;
+        acc0 += c0 * nbn;
+      } else {
+        acc += (p.M / C::kTileM) * nbn;
+      }
     }
     s_pref[p.G] = acc;
+    *s_total0 = acc0;
   }
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -644,16 +711,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   else cluster_sync_all();
   tc_fence_after();
   const uint32_t tmem_base = *s_tmem;
-  const int total = s_pref[p.G];
+  const int total0 = *s_total0;
+  const int total = s_pref[p.G] + total0;
 
   if (warp == 0) {
     if (lane == 0) {
       // ===== TMA producer (both CTAs of a pair load their halves) =====
       int stage = 0;
       uint32_t phase = 0;
+      bool arrived = p.flags == nullptr;
       for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
            tile = sched_tile(++w, unit, nunits)) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
+        if (t.remote && !arrived) {   // first tile with rows from other ranks
+          wait_arrivals(p);
+          arrived = true;
+        }
         for (int kb = 0; kb < t.nk; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = s_tiles + stage * C::kStageBytes;
@@ -688,7 +761,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
            tile = sched_tile(++w, unit, nunits)) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
+        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -735,7 +808,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
            tile = sched_tile(++w, unit, nunits)) {
-      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, tile);
+      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
       const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
@@ -1000,7 +1073,21 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
                                    int K, int b_major, int epilogue, int num_sms,
                                    int c_group_rows, int c_row_offset, void* stream,
                                    const long long* ret_map, const unsigned long long* ret_peers,
-                                   const RetMaps& rm);
+                                   const RetMaps& rm, const int32_t* self_rows = nullptr,
+                                   const int* flags = nullptr, int n_flags = 0,
+                                   const int* epoch = nullptr);
+
+extern "C" lz_status lz_grouped_gemm_arrival(const void* A, const void* B, void* C, void* aux,
+                                             int G, const int32_t* off, int rows_total, int N,
+                                             int K, int b_major, int epilogue, int num_sms,
+                                             const int32_t* self_rows, const int* flags,
+                                             int n_flags, const int* epoch, void* stream) {
+  if (!self_rows || !flags || !epoch || n_flags < 1) return LZ_ERR_ARG;
+  static const RetMaps none{};
+  return grouped_gemm_impl(0, A, B, C, aux, G, off, rows_total, 0, N, K, b_major, epilogue,
+                           num_sms, 0, 0, stream, nullptr, nullptr, none, self_rows, flags,
+                           n_flags, epoch);
+}
 
 extern "C" lz_status lz_grouped_gemm(int mode, const void* A, const void* B, void* C, void* aux,
                                      int G, const int32_t* off, int rows_total, int M, int N,
@@ -1035,7 +1122,8 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
                                    int K, int b_major, int epilogue, int num_sms,
                                    int c_group_rows, int c_row_offset, void* stream,
                                    const long long* ret_map, const unsigned long long* ret_peers,
-                                   const RetMaps& rm) {
+                                   const RetMaps& rm, const int32_t* self_rows, const int* flags,
+                                   int n_flags, const int* epoch) {
   if (G < 1 || !A || !B || !C || !off || rows_total < 0) return LZ_ERR_ARG;
   if (G > kMaxGroups) return LZ_ERR_UNSUPPORTED;
   if (epilogue < LZ_EPI_STORE || epilogue > LZ_EPI_DSWIGLU) return LZ_ERR_ARG;
@@ -1057,6 +1145,10 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
   p.aux = (__nv_bfloat16*)aux;
   p.ret_map = ret_map;
   p.ret_peers = ret_peers;
+  p.self_rows = self_rows;
+  p.flags = flags;
+  p.n_flags = n_flags;
+  p.epoch = epoch;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (sms < 2) sms = 2;

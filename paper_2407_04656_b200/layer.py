@@ -255,13 +255,20 @@ class _MoEFunction(torch.autograd.Function):
             cap = sym.rows
             X, Y = sym.buf(0), sym.buf(1)
             if layer.scatter:
+                # no barrier: each sender publishes an arrival flag after its dispatch and
+                # the first GEMM runs the tiles of our own rows while the rest arrive
+                ops.epoch_bump(sym.epoch)
                 ops.pack_p2p_ret(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X,
                                  plan.recv_m, plan.recv_off, sym.ret_ptrs, sym.ret, rank,
                                  plan.slot)
+                ops.signal_peers(sym.flag_peers[0], N, rank, sym.epoch)
+                self_rows = torch.stack([plan.recv_src_off[:, rank],
+                                         plan.recv_src_off[:, rank] + plan.recv_cnt[:, rank]],
+                                        1).index_select(0, layer._off_index[:-1]).contiguous()
             else:
                 ops.pack_p2p(x, plan.dest_rank, plan.dest_row, k, sym.peers(0), X, plan.recv_m,
                              plan.recv_off)
-            sym.barrier()
+                sym.barrier()
         else:
             # NCCL exchange: one D2H of the counts (+ error flag) per layer forward
             host = torch.cat([plan.send_sizes, plan.recv_counts, plan.err,
@@ -291,8 +298,12 @@ class _MoEFunction(torch.autograd.Function):
         A = torch.empty((cap, d_ff), dtype=torch.bfloat16, device=x.device)
         scatter = mode == "p2p" and layer.scatter
         if G > 0:
-            ops.grouped_gemm_rows(X, w1, off, A, aux=H,
-                                  epilogue=_lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU)
+            epi1 = _lib.LZ_EPI_SWIGLU if swi else _lib.LZ_EPI_GELU
+            if scatter:
+                ops.grouped_gemm_arrival(X, w1, off, A, self_rows, sym.flags[0], sym.epoch,
+                                         aux=H, epilogue=epi1)
+            else:
+                ops.grouped_gemm_rows(X, w1, off, A, aux=H, epilogue=epi1)
             if scatter:
                 # GEMM + combine all-to-all in one kernel: the epilogue stores every output
                 # row into its source rank's return buffer (row = source assignment)
@@ -325,6 +336,7 @@ class _MoEFunction(torch.autograd.Function):
         _mark(layer, "combine")
         ctx.layer = layer
         ctx.meta = (Tn, cap, sizes, mode, layer._fwd_version)
+        ctx.self_rows = self_rows if scatter else None
         ctx.plan = plan
         ctx.save_for_backward(x, wg, w1, w2, idx, w, probs, off, X, H, A, ret, row)
         return out
@@ -354,10 +366,11 @@ class _MoEFunction(torch.autograd.Function):
             if layer.scatter:
                 dw = ops.combine_bwd_p2p_ret(dout, ret, row, sym.peers(2), plan.dest_rank,
                                              plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
+                ops.signal_peers(sym.flag_peers[1], N, layer.rank, sym.epoch)
             else:
                 dw = ops.combine_bwd_p2p(dout, sym.peers(1), sym.peers(2), plan.dest_rank,
                                          plan.dest_row, w, k, dY, plan.recv_m, plan.recv_off)
-            sym.barrier()
+                sym.barrier()
         else:
             send_sizes, recv_counts, max_seg = sizes
             dret = torch.empty_like(ret)
@@ -380,9 +393,15 @@ class _MoEFunction(torch.autograd.Function):
         # streams, the remaining GEMMs leave `overlap_reserve` SMs free for them
         ov = max(2, (lzh_num_sms() - layer.overlap_reserve)) if N > 1 else 0
         if G > 0:
-            # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H)
-            ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
-                                  epilogue=_lib.LZ_EPI_DSWIGLU if swi else _lib.LZ_EPI_DGELU)
+            # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H); on N > 1 the
+            # tiles of our own rows start while the other ranks' dY rows arrive
+            epi2 = _lib.LZ_EPI_DSWIGLU if swi else _lib.LZ_EPI_DGELU
+            if mode == "p2p" and layer.scatter:
+                ops.grouped_gemm_arrival(dY, w2, off, dH, ctx.self_rows, sym.flags[1], sym.epoch,
+                                         b_major=_lib.LZ_MN_MAJOR, aux=H, epilogue=epi2)
+            else:
+                ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
+                                      epilogue=epi2)
             # variable-K weight gradients: dW2_e = dY_e^T A_e, dW1_e = dH_e^T X_e
             ops.grouped_gemm_wgrad(dY, A, off, dW2)
         if N > 1:

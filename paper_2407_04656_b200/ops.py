@@ -198,6 +198,29 @@ def grouped_gemm_scatter(A, B, off, C, ret_map, ret_peers, ret_peers_host, ret_r
     return C
 
 
+def grouped_gemm_arrival(A, B, off, C, self_rows, flags, epoch, *, b_major=_lib.LZ_K_MAJOR,
+                         epilogue=_lib.LZ_EPI_STORE, aux=None, num_sms: int = 0):
+    """grouped_gemm_rows whose tiles made of this rank's own rows (self_rows [G, 2]) run
+    first; the rest wait for the senders' arrival flags (flags [N] >= *epoch)."""
+    _cuda(A, B, off, C, self_rows, flags, epoch, aux)
+    rows, K = A.shape
+    G = off.numel() - 1
+    N = B.shape[1] if b_major == _lib.LZ_K_MAJOR else B.shape[2]
+    _gemm(ptr(A), ptr(B), ptr(C), ptr(aux), G, ptr(off), rows, N, K, b_major, epilogue, num_sms,
+          ptr(self_rows), ptr(flags), flags.numel(), ptr(epoch), _s(),
+          fn="lz_grouped_gemm_arrival")
+    return C
+
+
+def epoch_bump(epoch) -> None:
+    _lib.call("lz_epoch_bump", ptr(epoch), _s())
+
+
+def signal_peers(flag_peers, n: int, my_rank: int, epoch) -> None:
+    """Publish this step's epoch in every rank's arrival-flag slot for this sender."""
+    _lib.call("lz_signal_peers", ptr(flag_peers), int(n), int(my_rank), ptr(epoch), _s())
+
+
 def grouped_gemm_wgrad(A, B, off, C, num_sms: int = 0, c_group_rows: int = 0,
                        c_row_offset: int = 0):
     """C_g = A[off[g]:off[g+1]]^T . B[off[g]:off[g+1]]; A [rows, M], B [rows, N].
