@@ -350,9 +350,36 @@ def run_gpu(args, cfg):
     stages = {k2: round(v / nb, 4) for k2, v in stage_breakdown(layer.stage_events).items()}
     layer.stage_events = None
     stages_all = [stages]
+    nvlink = None
     if world > 1:
         stages_all = [None] * world
         dist.all_gather_object(stages_all, stages)
+        # NVLink evidence: off-rank bytes of the fused exchange kernels over their stage time,
+        # and the replica-group gradient all-reduce timed on its own (bus bandwidth)
+        remote = int((layer.last_plan.dest_rank != rank).sum()) * d * 2
+        gbps = {"dispatch": remote / (stages["dispatch"] * 1e-3) / 1e9,
+                "combine_bwd": remote / (stages["combine_bwd"] * 1e-3) / 1e9}
+        grads = [layer.w1.grad, layer.w2.grad]
+        bus_bytes = 0.0
+        for pg, pos in layer.replica_groups.buckets(layer.local_ids):
+            gsz = dist.get_world_size(pg)
+            per = sum(g_[0].numel() * g_.element_size() for g_ in grads) * len(pos)
+            bus_bytes += per * 2 * (gsz - 1) / gsz
+        layer.replica_groups.allreduce(grads, layer.local_ids)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(5):
+            layer.replica_groups.allreduce(grads, layer.local_ids)
+        a1.record()
+        torch.cuda.synchronize()
+        ar_ms = a0.elapsed_time(a1) / 5
+        mine = {"remote_MB": remote / 1e6, "dispatch_GBps": gbps["dispatch"],
+                "combine_bwd_GBps": gbps["combine_bwd"], "grad_allreduce_ms": ar_ms,
+                "grad_allreduce_busbw_GBps": bus_bytes / (ar_ms * 1e-3) / 1e9 if bus_bytes else 0.0}
+        nvlink = [None] * world
+        dist.all_gather_object(nvlink, mine)
 
     # ---- e2e through the public API: pinned host input -> device, result -> host.
     # Each step's x and upstream gradient are copied H2D on a side stream one step ahead
@@ -442,6 +469,13 @@ def run_gpu(args, cfg):
             "clocks": clk,
             "stages_ms_rank0": stages,
             "stages_ms_per_rank": stages_all if world > 1 else None,
+            "nvlink": None if nvlink is None else {
+                "per_rank": [{k2: round(v, 2) for k2, v in r.items()} for r in nvlink],
+                "link_peak_GBps_per_direction": 900,
+                "note": "dispatch / combine_bwd: off-rank bytes of the fused P2P kernels over "
+                        "their stage time (eager pass); grad all-reduce: NCCL replica-group "
+                        "all-reduce of the expert gradients timed alone (bus bandwidth); the "
+                        "scatter GEMMs' returns ride inside the GEMMs"},
             "exchange": layer.exchange_mode(),
         }
         if world == 1 and not args.no_cpu_baseline:
