@@ -416,6 +416,27 @@ def run_gpu(args, cfg):
 
     if rank == 0:
         hbm, tf_burst, tf_sus, src = _peaks()
+        # algorithmic HBM bytes per stage (SURVEY.md 8d formulas) over the stage's CUDA-event
+        # time in the eager breakdown pass (includes launch gaps: a lower bound on the
+        # kernels' own GB/s; ncu per-kernel numbers are in profiles/)
+        Pa = Tn * k
+        stage_bytes = {
+            "gate": Tn * d * 2 + E * d * 2 + Tn * E * 4 + Tn * k * 8,
+            "plan": Pa * 4 + Pa * 16,
+            "dispatch": Tn * d * 2 + Pa * d * 2 + Pa * 4,
+            "combine": Pa * d * 2 + Pa * 8 + Tn * d * 2,
+            "combine_bwd": Tn * d * 2 + 2 * Pa * d * 2 + Pa * 8,
+            "dispatch_bwd": Pa * d * 2 + Tn * d * 2 + 2 * Tn * E * 4,
+            "router_wgrad": Tn * d * 2 + Tn * E * 4,
+        }
+        hbm_stages = {}
+        if world == 1:
+            for st_name, nbytes in stage_bytes.items():
+                ms_st = stages.get(st_name)
+                if ms_st:
+                    gbs = nbytes / (ms_st * 1e-3) / 1e9
+                    hbm_stages[st_name] = {"MB": round(nbytes / 1e6, 1), "ms": round(ms_st, 4),
+                                           "GBps": round(gbs, 1), "frac": round(gbs / hbm, 3)}
         P = Tn * k
         gemms_per_step = 6 if cfg["bwd"] else 2
         n_mat = 3 if act == "swiglu" else 2
@@ -468,6 +489,7 @@ def run_gpu(args, cfg):
             "gpu_launches": launches,
             "clocks": clk,
             "stages_ms_rank0": stages,
+            "hbm_stages": hbm_stages or None,
             "stages_ms_per_rank": stages_all if world > 1 else None,
             "nvlink": None if nvlink is None else {
                 "per_rank": [{k2: round(v, 2) for k2, v in r.items()} for r in nvlink],
