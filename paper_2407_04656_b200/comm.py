@@ -111,15 +111,25 @@ class ReplicaGroups:
     as torch.distributed requires) once per plan; experts sharing an owner set share
     a communicator and their gradients travel in one bucket."""
 
-    def __init__(self, R: Sequence[Sequence[int]], group=None, backend: str | None = None):
+    def __init__(self, R: Sequence[Sequence[int]], group=None, backend: str | None = None,
+                 max_ctas: int | None = None):
+        """max_ctas (NCCL): cap on the CTAs each all-reduce may occupy -- the backward GEMMs
+        that overlap the all-reduces leave exactly that many SMs free, so the persistent
+        GEMM CTAs and NCCL's never queue behind each other."""
         self.rank, self.n = world(group)
         self.owners = owner_sets(R)
         self.sets = sorted({o for o in self.owners if len(o) > 1})
         self.groups: dict[tuple[int, ...], object] = {}
         if self.n > 1:
             base = dist.get_process_group_ranks(group) if group is not None else list(range(self.n))
+            opts = None
+            if max_ctas and (backend or dist.get_backend(group)) == "nccl":
+                opts = dist.ProcessGroupNCCL.Options()
+                opts.config.max_ctas = int(max_ctas)
+                opts.config.min_ctas = 1
+                opts.is_high_priority_stream = True
             for s in self.sets:
-                pg = dist.new_group([base[j] for j in s], backend=backend)
+                pg = dist.new_group([base[j] for j in s], backend=backend, pg_options=opts)
                 if self.rank in s:
                     self.groups[s] = pg
 

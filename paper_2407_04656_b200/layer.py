@@ -153,7 +153,11 @@ class MoELayer(torch.nn.Module):
         # blocks [2 d_ff, d];  w2[g] = W2_e [d, d_ff] (row-major, K contiguous for fwd)
         self.w1 = torch.nn.Parameter(torch.stack(w1s).contiguous())
         self.w2 = torch.nn.Parameter(torch.stack(w2s).contiguous())
-        self.replica_groups = comm.ReplicaGroups(R, self.group) if self.world > 1 else None
+        # LZ_NCCL_MAX_CTAS caps the CTAs of the replica-group all-reduces (0: NCCL default);
+        # 32 measured best next to the GEMMs that leave LZ_OVERLAP_SMS SMs free (cfg3, N=2)
+        max_ctas = int(os.environ.get("LZ_NCCL_MAX_CTAS", "32")) or None
+        self.replica_groups = (comm.ReplicaGroups(R, self.group, max_ctas=max_ctas)
+                               if self.world > 1 else None)
 
     def exchange_mode(self) -> str:
         """'local' (N = 1), 'p2p' (fused NVLink dispatch/combine through symmetric memory,
@@ -402,14 +406,15 @@ class _MoEFunction(torch.autograd.Function):
             else:
                 ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
                                       epilogue=epi2)
-            # variable-K weight gradients: dW2_e = dY_e^T A_e, dW1_e = dH_e^T X_e
-            ops.grouped_gemm_wgrad(dY, A, off, dW2)
-        if N > 1:
-            works += layer.replica_groups.allreduce_async([dW2], layer.local_ids)
-        if G > 0:
-            ops.grouped_gemm_wgrad(dH, X, off, dW1, num_sms=ov)
+            # variable-K weight gradients: dW1_e = dH_e^T X_e first -- the larger all-reduce
+            # (2x for SwiGLU's W1|W3) then overlaps two GEMMs -- then dW2_e = dY_e^T A_e
+            ops.grouped_gemm_wgrad(dH, X, off, dW1)
         if N > 1:
             works += layer.replica_groups.allreduce_async([dW1], layer.local_ids)
+        if G > 0:
+            ops.grouped_gemm_wgrad(dY, A, off, dW2, num_sms=ov)
+        if N > 1:
+            works += layer.replica_groups.allreduce_async([dW2], layer.local_ids)
         scatter = mode == "p2p" and layer.scatter
         if G > 0:
             # dX = dH . W1 (W1_e [d_ff, d] read MN-major); scatter: rows go back to their
