@@ -370,6 +370,9 @@ struct TileInfo {
 };
 
 template <int CG>
+__host__ __device__ constexpr int C_TILE_M() { return BM * CG; }
+
+template <int CG>
 __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
                                                 const int32_t* s_off, const int32_t* s_perm,
                                                 int total0, int tile) {
@@ -411,8 +414,18 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
     t.nk = p.K / BK;
     t.remote = p.self_rows != nullptr;
   } else {
+    // weight gradient: raster along the smaller output dimension so the concurrently
+    // running tiles share the operand slices of the larger one (cfg3 dW2 = dY^T A with
+    // M = 4096, N = 14336: N-fastest order streamed A's 256-column slices from DRAM once
+    // per m-block)
+    const int nbm = p.M / C_TILE_M<CG>();
     t.g = s_perm[lo];
-    t.mb = local / nbn;
+    if (nbm <= nbn) {
+      t.mb = local % nbm;
+      t.nb = local / nbm;
+    } else {
+      t.mb = local / nbn;
+    }
     t.nk = (s_off[t.g + 1] - s_off[t.g]) / BK;
   }
   return t;

@@ -36,13 +36,17 @@ def main():
     ap.add_argument("lib_b")
     ap.add_argument("--swiglu", action="store_true")
     ap.add_argument("--trials", type=int, default=15)
+    ap.add_argument("--groups", type=int, default=16)
+    ap.add_argument("--d", type=int, default=1024)
+    ap.add_argument("--dff", type=int, default=4096)
+    ap.add_argument("--rows", type=int, default=131072)
     a = ap.parse_args()
     libs = [load(a.lib_a), load(a.lib_b)]
-    G, d, dff = 16, 1024, 4096
+    G, d, dff = a.groups, a.d, a.dff
     torch.manual_seed(0)
     # Zipf(1.2)-like group sizes (the cfg2 routing), 256-row padded
     w = torch.tensor([(1 + e) ** -1.2 for e in range(G)])
-    m = [int(v) // 256 * 256 + 256 for v in (w / w.sum() * 131072)]
+    m = [int(v) // 256 * 256 + 256 for v in (w / w.sum() * a.rows)]
     off = torch.tensor([0] + torch.tensor(m).cumsum(0).tolist(), dtype=torch.int32, device="cuda")
     rows = int(off[-1])
     f1 = 2 * dff if a.swiglu else dff
