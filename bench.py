@@ -475,6 +475,8 @@ def run_gpu(args, cfg):
             "roofline": {"kernel": "lz grouped_gemm (tcgen05 fwd+dgrad+wgrad)", "bound": "tensor",
                          "achieved": achieved, "peak": tf_sus, "unit": "TFLOP/s",
                          "frac": achieved / tf_sus, "traffic": traffic,
+                         "traffic_unit": "DRAM bytes per GEMM launch (ncu --set full, "
+                                         "profiles/gemm_traffic.json)",
                          "peak_kind": f"{src} sustained bf16",
                          "flops_per_launch": flops_per_launch,
                          "gemm_ms_per_step": gemm_ms / args.steps,
