@@ -104,6 +104,9 @@ def owner_sets(R: Sequence[Sequence[int]]) -> list[tuple[int, ...]]:
     return [tuple(j for j, v in enumerate(row) if v > 0) for row in R]
 
 
+_PG_CACHE: dict = {}
+
+
 class ReplicaGroups:
     """Sub-communicators for the replica-group gradient all-reduce.
 
@@ -128,8 +131,15 @@ class ReplicaGroups:
                 opts.config.max_ctas = int(max_ctas)
                 opts.config.min_ctas = 1
                 opts.is_high_priority_stream = True
+            parent = getattr(group, "group_name", "default") if group is not None else "default"
             for s in self.sets:
-                pg = dist.new_group([base[j] for j in s], backend=backend, pg_options=opts)
+                # communicators are cached per (parent group, member set): a re-plan that
+                # keeps an owner set reuses its communicator instead of leaking a new one
+                key = (parent, tuple(base[j] for j in s), backend, max_ctas)
+                pg = _PG_CACHE.get(key)
+                if pg is None:
+                    pg = dist.new_group([base[j] for j in s], backend=backend, pg_options=opts)
+                    _PG_CACHE[key] = pg
                 if self.rank in s:
                     self.groups[s] = pg
 
