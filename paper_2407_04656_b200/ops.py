@@ -296,9 +296,5 @@ def combine_bwd_p2p_ret(dout, y_ret, y_row, peers_dy, dest_rank, dest_row, w, k:
     return dw
 
 
-def set_gemm_direct_epilogue(on: int) -> int:
-    return int(_lib.raw("lz_gemm_set_direct_epilogue", int(on)))
-
-
 if "LZ_GEMM_CTA" in __import__("os").environ:  # A/B switch for the GEMM variant
     set_gemm_cta_group(int(__import__("os").environ["LZ_GEMM_CTA"]))

@@ -47,3 +47,8 @@ t(lambda: ops.combine_bwd(dout, y, rows.view(-1), w, k, dy), "combine_bwd",
   Tn * d * 2 + 2 * P * d * 2 + P * 8)
 t(lambda: ops.dispatch_bwd(dxe, rows.view(-1), probs, idx, dw, None, False, Tn),
   "dispatch_bwd (no router term)", P * d * 2 + Tn * d * 2 + 2 * Tn * E * 4)
+seq_rows = torch.arange(P, dtype=torch.int32, device="cuda")
+t(lambda: ops.dispatch_bwd(dxe, seq_rows, probs, idx, dw, None, False, Tn),
+  "dispatch_bwd (no router term, sequential rows)", P * d * 2 + Tn * d * 2 + 2 * Tn * E * 4)
+t(lambda: ops.combine_bwd(dout, y, seq_rows, w, k, dy), "combine_bwd (sequential rows)",
+  Tn * d * 2 + 2 * P * d * 2 + P * 8)
