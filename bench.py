@@ -124,6 +124,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_reference(cfg, n_ranks, tokens_per_rank, reps, threads, seed=0):
     """Reference path on the host cores (oracle port).  Returns (tokens/s, seconds, tokens)."""
     from oracle import cpu_path
@@ -166,6 +176,7 @@ def run_reference(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": cfg["name"], "sample_tokens_per_step": tok // args.steps},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{tok // args.steps} tokens per step x {args.steps} steps"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -508,6 +519,7 @@ def run_gpu(args, cfg):
             reps = cfg.get("cpu_reps", args.cpu_reps)
             tps, dt, tok = cpu_reference(cfg, 1, ctok, reps, threads)
             line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": threads,
+                                    "cpu_model": cpu_model(),
                                     "kind": "port",
                                     "sample": f"{tok} tokens ({reps} x {ctok}) of the "
                                               f"same layer {'fwd+bwd' if cfg['bwd'] else 'fwd'} "
@@ -597,7 +609,7 @@ def run_virtual(args, cfg):
         cpu_reference(cfg, nv, Tn, 1, threads)
         vals = [cpu_reference(cfg, nv, Tn, 1, threads) for _ in range(max(1, args.cpu_reps // 4))]
         cpu = {"value": sum(v[2] for v in vals) / sum(v[1] for v in vals), "unit": "tokens/s",
-               "cores": threads, "kind": "port",
+               "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                "sample": f"full config 1 ({tokens} tokens, 4 simulated ranks) x {len(vals)}"}
     flops = 2 * tokens * k * d * dff * 2
     line = {"metric": METRIC.replace("fwd+bwd", "fwd"), "value": tokens / (ms * 1e-3),
