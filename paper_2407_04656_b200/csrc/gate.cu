@@ -14,15 +14,21 @@
 namespace lz {
 
 // Softmax + top-k for one token whose E logits are at `lg` (smem or global).
-__device__ __forceinline__ void finish_token(const float* lg, int E, int k, int renorm,
-                                             int32_t* __restrict__ idx_out,
-                                             float* __restrict__ w_out,
-                                             float* __restrict__ probs_out,
-                                             int32_t* s_hist) {
-  int sel[LZ_MAX_TOPK];
-  float sv[LZ_MAX_TOPK];
+// KK > 0: compile-time k (the running top-k lives in registers); KK == 0: any k <= 8.
+// Insertion keeps the list sorted by value; a new value is inserted only when strictly
+// greater than an entry, so ties keep the lower expert id.
+template <int KK>
+__device__ __forceinline__ void finish_token_k(const float* lg, int E, int k, int renorm,
+                                               int32_t* __restrict__ idx_out,
+                                               float* __restrict__ w_out,
+                                               float* __restrict__ probs_out,
+                                               int32_t* s_hist) {
+  constexpr int KM = KK > 0 ? KK : LZ_MAX_TOPK;
+  const int kk = KK > 0 ? KK : k;
+  int sel[KM];
+  float sv[KM];
 #pragma unroll
-  for (int s = 0; s < LZ_MAX_TOPK; ++s) {
+  for (int s = 0; s < KM; ++s) {
     sel[s] = -1;
     sv[s] = -INFINITY;
   }
@@ -30,9 +36,26 @@ __device__ __forceinline__ void finish_token(const float* lg, int E, int k, int 
   for (int e = 0; e < E; ++e) {
     const float v = lg[e];
     mx = fmaxf(mx, v);
-    // insertion into the running top-k: strictly greater wins, so ties keep the lower id
-    if (v > sv[k - 1] || sel[k - 1] < 0) {
-      int pos = k - 1;
+    if (KK > 0) {
+      // carry insertion over compile-time positions (registers only)
+      bool ins = false;
+      float cv = v;
+      int ci = e;
+#pragma unroll
+      for (int p = 0; p < KM; ++p) {
+        const bool here = !ins && (cv > sv[p] || sel[p] < 0);
+        if (ins || here) {
+          const float tv = sv[p];
+          const int ti = sel[p];
+          sv[p] = cv;
+          sel[p] = ci;
+          cv = tv;
+          ci = ti;
+          ins = true;
+        }
+      }
+    } else if (v > sv[kk - 1] || sel[kk - 1] < 0) {
+      int pos = kk - 1;
       while (pos > 0 && (v > sv[pos - 1] || sel[pos - 1] < 0)) {
         sv[pos] = sv[pos - 1];
         sel[pos] = sel[pos - 1];
@@ -47,18 +70,34 @@ __device__ __forceinline__ void finish_token(const float* lg, int E, int k, int 
   const float inv = 1.f / sum;
   if (probs_out)
     for (int e = 0; e < E; ++e) probs_out[e] = expf(lg[e] - mx) * inv;
-  float ps[LZ_MAX_TOPK];
+  float ps[KM];
   float psum = 0.f;
-  for (int s = 0; s < k; ++s) {
-    ps[s] = expf(sv[s] - mx) * inv;
-    psum += ps[s];
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    if (s < kk) {
+      ps[s] = expf(sv[s] - mx) * inv;
+      psum += ps[s];
+    }
   }
   const float rn = renorm ? 1.f / psum : 1.f;
-  for (int s = 0; s < k; ++s) {
-    idx_out[s] = sel[s];
-    w_out[s] = ps[s] * rn;
-    atomicAdd(&s_hist[sel[s]], 1);
+#pragma unroll
+  for (int s = 0; s < KM; ++s) {
+    if (s < kk) {
+      idx_out[s] = sel[s];
+      w_out[s] = ps[s] * rn;
+      atomicAdd(&s_hist[sel[s]], 1);
+    }
   }
+}
+
+__device__ __forceinline__ void finish_token(const float* lg, int E, int k, int renorm,
+                                             int32_t* __restrict__ idx_out,
+                                             float* __restrict__ w_out,
+                                             float* __restrict__ probs_out,
+                                             int32_t* s_hist) {
+  if (k == 2) finish_token_k<2>(lg, E, k, renorm, idx_out, w_out, probs_out, s_hist);
+  else if (k == 1) finish_token_k<1>(lg, E, k, renorm, idx_out, w_out, probs_out, s_hist);
+  else finish_token_k<0>(lg, E, k, renorm, idx_out, w_out, probs_out, s_hist);
 }
 
 __global__ void __launch_bounds__(256) gate_topk_kernel(const float* __restrict__ logits, int Tn,
