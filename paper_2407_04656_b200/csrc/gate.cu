@@ -169,27 +169,56 @@ __global__ void __launch_bounds__(32 * kRouterWarps) router_gate_kernel(
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
   const uint4 zero = make_uint4(0, 0, 0, 0);
-  constexpr int U = NT <= 2 ? 4 : (NT <= 4 ? 2 : 1);  // k chunks in flight
-  for (int kb = 0; kb < d; kb += 32 * U) {
-    // all loads of the U chunks first (x rows and the router weights), then the MMAs
-    uint4 xa[U], xb[U], bw[U][NT];
+  if constexpr (NT <= 2) {
+    constexpr int U = 4;  // k chunks in flight
+    for (int kb = 0; kb < d; kb += 32 * U) {
+      // all loads of the U chunks first (x rows and the router weights), then the MMAs
+      uint4 xa[U], xb[U], bw[U][NT];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + 32 * u;
-      const bool in = kk < d;
-      xa[u] = (v0 && in) ? ld_nc_v4(x0 + kk) : zero;
-      xb[u] = (v1 && in) ? ld_nc_v4(x1 + kk) : zero;
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        const bool in = kk < d;
+        xa[u] = (v0 && in) ? ld_nc_v4(x0 + kk) : zero;
+        xb[u] = (v1 && in) ? ld_nc_v4(x1 + kk) : zero;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) bw[u][nt] = (wv[nt] && in) ? ld_v4(wrow[nt] + kk) : zero;
+        for (int nt = 0; nt < NT; ++nt) bw[u][nt] = (wv[nt] && in) ? ld_v4(wrow[nt] + kk) : zero;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        if (kk >= d) break;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma_bf16_16816(acc[nt], xa[u].x, xb[u].x, xa[u].y, xb[u].y, bw[u][nt].x, bw[u][nt].y);
+          mma_bf16_16816(acc[nt], xa[u].z, xb[u].z, xa[u].w, xb[u].w, bw[u][nt].z, bw[u][nt].w);
+        }
+      }
     }
+  } else {
+    // wide routers (E > 16): the x rows (HBM) stay U = 4 chunks ahead; the router weights
+    // (L1/L2-resident, shared by every warp) are fetched per chunk, right before its MMAs
+    constexpr int U = 4;
+    for (int kb = 0; kb < d; kb += 32 * U) {
+      uint4 xa[U], xb[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int kk = kb + 32 * u;
-      if (kk >= d) break;
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        const bool in = kk < d;
+        xa[u] = (v0 && in) ? ld_nc_v4(x0 + kk) : zero;
+        xb[u] = (v1 && in) ? ld_nc_v4(x1 + kk) : zero;
+      }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        mma_bf16_16816(acc[nt], xa[u].x, xb[u].x, xa[u].y, xb[u].y, bw[u][nt].x, bw[u][nt].y);
-        mma_bf16_16816(acc[nt], xa[u].z, xb[u].z, xa[u].w, xb[u].w, bw[u][nt].z, bw[u][nt].w);
+      for (int u = 0; u < U; ++u) {
+        const int kk = kb + 32 * u;
+        if (kk >= d) break;
+        uint4 bw[NT];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) bw[nt] = wv[nt] ? ld_v4(wrow[nt] + kk) : zero;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          mma_bf16_16816(acc[nt], xa[u].x, xb[u].x, xa[u].y, xb[u].y, bw[nt].x, bw[nt].y);
+          mma_bf16_16816(acc[nt], xa[u].z, xb[u].z, xa[u].w, xb[u].w, bw[nt].z, bw[nt].w);
+        }
       }
     }
   }

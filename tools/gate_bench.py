@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2407_04656_b200 import _lib  # noqa: E402
 
-Tn, d, E, k = 65536, 1024, 16, 2
+Tn, d, E, k = (int(v) for v in os.environ.get("GATE_SHAPE", "65536,1024,16,2").split(","))
 x = torch.randn(Tn, d, device="cuda").bfloat16()
 wg = (torch.randn(E, d, device="cuda") * 0.04).bfloat16()
 bg = torch.zeros(E, device="cuda")
@@ -34,4 +34,6 @@ for path in sys.argv[1:]:
         if i >= 2:
             ts.append(a.elapsed_time(b) * 1e3)
     ts.sort()
-    print(f"{path}: min {ts[0]:.1f} med {ts[len(ts)//2]:.1f} us  ({134.2e6 / (ts[0] * 1e-6) / 1e12:.2f} TB/s)")
+    nbytes = Tn * d * 2
+    print(f"{path} [{Tn}x{d}, E{E} k{k}]: min {ts[0]:.1f} med {ts[len(ts)//2]:.1f} us  "
+          f"({nbytes / (ts[0] * 1e-6) / 1e12:.2f} TB/s)")
