@@ -100,19 +100,101 @@ __device__ __forceinline__ void finish_token(const float* lg, int E, int k, int 
   else finish_token_k<0>(lg, E, k, renorm, idx_out, w_out, probs_out, s_hist);
 }
 
+// Logits staged through shared memory with coalesced loads (a block owns `tpb` whole
+// logit rows, tpb * E <= 16K floats), then one thread per token runs the softmax/top-k on
+// its (padded) smem row -- direct per-thread row reads were 32-way uncoalesced.
 __global__ void __launch_bounds__(256) gate_topk_kernel(const float* __restrict__ logits, int Tn,
-                                                        int E, int k, int renorm,
+                                                        int E, int k, int renorm, int tpb,
                                                         int32_t* __restrict__ idx,
                                                         float* __restrict__ w,
                                                         float* __restrict__ probs,
                                                         int32_t* __restrict__ hist) {
-  extern __shared__ int32_t s_hist[];
+  extern __shared__ float g_smem[];
+  const int ld = E + 1;                                   // padded row (bank spread)
+  float* s_lg = g_smem;                                   // [tpb][E + 1]
+  int32_t* s_hist = reinterpret_cast<int32_t*>(g_smem + (size_t)tpb * ld);
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
+  const long t0 = (long)blockIdx.x * tpb;
+  const int nt = (int)min((long)tpb, (long)Tn - t0);
+  const float* src = logits + t0 * E;
+  {
+    // warp per row, coalesced, asynchronous (cp.async: no register round trip, so the
+    // loads of all rows are in flight together), no index division
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(s_lg);
+    for (int r = threadIdx.x >> 5; r < nt; r += nw)
+      for (int e = lane; e < E; e += 32)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s0 + (uint32_t)(r * ld + e) * 4u),
+                     "l"(src + (size_t)r * E + e)
+                     : "memory");
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
   __syncthreads();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < Tn)
-    finish_token(logits + (size_t)t * E, E, k, renorm, idx + (size_t)t * k, w + (size_t)t * k,
-                 probs ? probs + (size_t)t * E : nullptr, s_hist);
+  if (E >= 16 && k <= 2) {
+    // 8 lanes per token, each over every 8th expert: local max / sum / top-2, then
+    // butterfly merges (ties -> lower id, as the sequential insertion)
+    constexpr int L = 8;
+    const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+    const unsigned gmask = 0xffffffffu;
+    for (int ti0 = threadIdx.x / L; ti0 < ((nt + 3) & ~3); ti0 += blockDim.x / L) {
+      // every lane of the warp iterates together (shuffles need the full warp)
+      const bool live = ti0 < nt;
+      const float* lg = s_lg + (size_t)(live ? ti0 : 0) * ld;
+      float v1 = -INFINITY, v2 = -INFINITY, mx = -INFINITY;
+      int i1 = 0x7fffffff, i2 = 0x7fffffff;
+      for (int e = sub; e < E; e += L) {
+        const float v = lg[e];
+        mx = fmaxf(mx, v);
+        if (v > v1) { v2 = v1; i2 = i1; v1 = v; i1 = e; }
+        else if (v > v2) { v2 = v; i2 = e; }
+      }
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(gmask, mx, o));
+        const float w1 = __shfl_xor_sync(gmask, v1, o), w2 = __shfl_xor_sync(gmask, v2, o);
+        const int j1 = __shfl_xor_sync(gmask, i1, o), j2 = __shfl_xor_sync(gmask, i2, o);
+        // merge two (value desc, id asc) sorted pairs
+        auto better = [](float a, int ia, float b, int ib) { return a > b || (a == b && ia < ib); };
+        float r1, r2;
+        int q1, q2;
+        if (better(v1, i1, w1, j1)) {
+          r1 = v1; q1 = i1;
+          if (better(v2, i2, w1, j1)) { r2 = v2; q2 = i2; } else { r2 = w1; q2 = j1; }
+        } else {
+          r1 = w1; q1 = j1;
+          if (better(v1, i1, w2, j2)) { r2 = v1; q2 = i1; } else { r2 = w2; q2 = j2; }
+        }
+        v1 = r1; i1 = q1; v2 = r2; i2 = q2;
+      }
+      float sum = 0.f;
+      for (int e = sub; e < E; e += L) sum += expf(lg[e] - mx);
+#pragma unroll
+      for (int o = 1; o < L; o <<= 1) sum += __shfl_xor_sync(gmask, sum, o);
+      if (!live) continue;
+      const float inv = 1.f / sum;
+      const long t = t0 + ti0;
+      if (probs)
+        for (int e = sub; e < E; e += L) probs[t * E + e] = expf(lg[e] - mx) * inv;
+      if (sub == 0) {
+        const float p1 = expf(v1 - mx) * inv, p2 = k == 2 ? expf(v2 - mx) * inv : 0.f;
+        const float rn = renorm ? 1.f / (p1 + p2) : 1.f;
+        idx[t * k] = i1;
+        w[t * k] = p1 * rn;
+        atomicAdd(&s_hist[i1], 1);
+        if (k == 2) {
+          idx[t * k + 1] = i2;
+          w[t * k + 1] = p2 * rn;
+          atomicAdd(&s_hist[i2], 1);
+        }
+      }
+    }
+  } else {
+    for (int ti = threadIdx.x; ti < nt; ti += blockDim.x) {
+      const long t = t0 + ti;
+      finish_token(s_lg + (size_t)ti * ld, E, k, renorm, idx + t * k, w + t * k,
+                   probs ? probs + t * E : nullptr, s_hist);
+    }
+  }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x)
     if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
@@ -257,8 +339,18 @@ extern "C" lz_status lz_gate_topk(const float* logits, int Tn, int E, int k, int
   if (cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess) return lzh::check_launch();
   if (Tn == 0) return LZ_OK;
   if (!logits || !idx || !w) return LZ_ERR_ARG;
-  gate_topk_kernel<<<(Tn + 255) / 256, 256, sizeof(int32_t) * E, s>>>(logits, Tn, E, k, renorm,
-                                                                     idx, w, probs, hist);
+  int tpb = 16384 / (E + 1);
+  tpb = tpb > 256 ? 256 : (tpb < 1 ? 1 : tpb);
+  const size_t smem = sizeof(float) * (size_t)tpb * (E + 1) + sizeof(int32_t) * E;
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(gate_topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             80 * 1024) != cudaSuccess)
+      return lzh::check_launch();
+    attr = true;
+  }
+  gate_topk_kernel<<<(int)((Tn + tpb - 1) / tpb), 256, smem, s>>>(logits, Tn, E, k, renorm, tpb,
+                                                                  idx, w, probs, hist);
   return lzh::check_launch();
 }
 

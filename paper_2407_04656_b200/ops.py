@@ -50,13 +50,13 @@ def router_gate(x, wg, bias, k: int, renorm: bool = False, probs: bool = True):
     return idx, w, pr, hist
 
 
-def gate_topk(logits, k: int, renorm: bool = False):
+def gate_topk(logits, k: int, renorm: bool = False, probs: bool = True):
     _cuda(logits)
     Tn, E = logits.shape
     dev = logits.device
     idx = torch.empty((Tn, k), dtype=torch.int32, device=dev)
     w = torch.empty((Tn, k), dtype=torch.float32, device=dev)
-    pr = torch.empty((Tn, E), dtype=torch.float32, device=dev)
+    pr = torch.empty((Tn, E), dtype=torch.float32, device=dev) if probs else None
     hist = torch.empty(E, dtype=torch.int32, device=dev)
     _lib.call("lz_gate_topk", ptr(logits.float().contiguous()), Tn, E, k, int(renorm), ptr(idx),
               ptr(w), ptr(pr), ptr(hist), _s())

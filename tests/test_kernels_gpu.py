@@ -23,7 +23,10 @@ def _close(got, ref, rtol=8e-3, atol_scale=1e-3):
 
 
 @pytest.mark.parametrize("Tn,E,k,renorm", [(1000, 16, 2, False), (4096, 8, 2, True),
-                                           (333, 64, 1, False), (64, 5, 3, True)])
+                                           (333, 64, 1, False), (64, 5, 3, True),
+                                           (100000, 64, 2, False), (5000, 1024, 2, True),
+                                           (777, 33, 1, False), (256, 16, 2, True),
+                                           (300, 64, 4, False)])
 def test_gate_topk_exact_ids(Tn, E, k, renorm):
     g = torch.Generator().manual_seed(Tn + E)
     logits = torch.randn(Tn, E, generator=g)
