@@ -698,8 +698,24 @@ def run_dispatch_sweep(args, cfg):
         t_gate, t_plan, t_pack, t_comb = (a / reps for a in acc)
         pack_b = Tn * d * 2 + P * d * 2 + P * 4
         comb_b = P * d * 2 + P * 8 + Tn * d * 2
-        total = t_gate + t_plan + t_pack + t_comb
+        # the step itself as one CUDA graph (device time; the per-stage events above run
+        # eagerly and include each small stage's host launch latency)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            once(False)
+        for _ in range(3):
+            graph.replay()
+        torch.cuda.synchronize()
+        ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ga.record()
+        for _ in range(reps):
+            graph.replay()
+        gb.record()
+        torch.cuda.synchronize()
+        total = ga.elapsed_time(gb) / reps
+        del graph
         sweep.append({"tokens": Tn, "ms": round(total, 4), "tokens_per_s": Tn / (total * 1e-3),
+                      "eager_stage_sum_ms": round(t_gate + t_plan + t_pack + t_comb, 4),
                       "gate_ms": round(t_gate, 4), "plan_ms": round(t_plan, 4),
                       "pack_ms": round(t_pack, 4), "combine_ms": round(t_comb, 4),
                       "pack_GBps": pack_b / (t_pack * 1e-3) / 1e9,
