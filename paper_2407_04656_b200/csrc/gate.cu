@@ -326,6 +326,127 @@ __global__ void __launch_bounds__(32 * kRouterWarps) router_gate_kernel(
     if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
 }
 
+// ---------------------------------------------------------------------------
+// Wide routers (E > 16, d % 64 == 0): the register-direct kernel above has every warp
+// re-read all of Wg (E x d x 2 bytes, 256 KB at E = 64, d = 2048 -- too big for L1), so
+// the router weights dominate L2 traffic.  Here a block of 8 warps x 16 tokens streams
+// x and Wg through a 4-stage cp.async ring of 64-column chunks shared by all its warps
+// (A fragments by ldmatrix); the logits tile is then staged in the idle ring.
+// ---------------------------------------------------------------------------
+constexpr int kRgK = 64;                  // columns per stage
+constexpr int kRgStages = 4;
+constexpr int kRgXRow = kRgK + 8;         // bf16 per smem row (144 B: ldmatrix conflict-free)
+template <int NT>
+struct RgCfg {
+  static constexpr int kXBytes = kRouterTok * kRgXRow * 2;
+  static constexpr int kWBytes = NT * 8 * kRgXRow * 2;
+  static constexpr int kStage = kXBytes + kWBytes;
+  static constexpr int kSmem = kRgStages * kStage;
+  static_assert(kRouterWarps * 16 * (NT * 8 + 1) * 4 <= kSmem, "logit tile fits the ring");
+};
+__device__ __forceinline__ void rg_cp16(uint32_t dst, const void* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(ok ? 16 : 0));
+}
+template <int NT>
+__global__ void __launch_bounds__(32 * kRouterWarps, 2) router_gate_pipe(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int Tn, int d, int E, int k, int renorm,
+    int32_t* __restrict__ idx, float* __restrict__ w, float* __restrict__ probs,
+    int32_t* __restrict__ hist) {
+  using C = RgCfg<NT>;
+  extern __shared__ __align__(16) uint8_t rg_smem[];
+  __shared__ int32_t s_hist[NT * 8];
+  for (int e = threadIdx.x; e < NT * 8; e += blockDim.x) s_hist[e] = 0;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int g = lane >> 2, tq = lane & 3;
+  const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(rg_smem);
+  const int nk = d / kRgK;
+  const int nblocks = (Tn + kRouterTok - 1) / kRouterTok;
+  for (int tb = blockIdx.x; tb < nblocks; tb += gridDim.x) {
+    const long tok0 = (long)tb * kRouterTok;
+    auto stage = [&](int buf, int kc) {
+      const uint32_t sx = s0 + buf * C::kStage, sw = sx + C::kXBytes;
+      for (int q = threadIdx.x; q < kRouterTok * 8; q += blockDim.x) {
+        const int r = q >> 3, c = q & 7;
+        const long t = tok0 + r;
+        rg_cp16(sx + (r * kRgXRow + c * 8) * 2, x + (t < Tn ? t : 0) * d + kc * kRgK + c * 8,
+                t < Tn);
+      }
+      for (int q = threadIdx.x; q < NT * 8 * 8; q += blockDim.x) {
+        const int e = q >> 3, c = q & 7;
+        rg_cp16(sw + (e * kRgXRow + c * 8) * 2,
+                wg + (e < E ? e : 0) * (long)d + kc * kRgK + c * 8, e < E);
+      }
+      asm volatile("cp.async.commit_group;");
+    };
+#pragma unroll
+    for (int i = 0; i < kRgStages - 1; ++i) {
+      if (i < nk) stage(i, i);
+      else asm volatile("cp.async.commit_group;");
+    }
+    float acc[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+    for (int kc = 0; kc < nk; ++kc) {
+      const int buf = kc % kRgStages;
+      asm volatile("cp.async.wait_group %0;" ::"n"(kRgStages - 2) : "memory");
+      __syncthreads();
+      {
+        const int j = kc + kRgStages - 1;
+        if (j < nk) stage(j % kRgStages, j);
+        else asm volatile("cp.async.commit_group;");
+      }
+      const uint32_t sx = s0 + buf * C::kStage;
+      const __nv_bfloat16* wsm =
+          reinterpret_cast<const __nv_bfloat16*>(rg_smem + buf * C::kStage + C::kXBytes);
+#pragma unroll
+      for (int kk = 0; kk < kRgK / 16; ++kk) {
+        uint32_t a0, a1, a2, a3;
+        const uint32_t aaddr =
+            sx + ((warp * 16 + (lane & 15)) * kRgXRow + kk * 16 + (lane >> 4) * 8) * 2;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                     : "r"(aaddr));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const __nv_bfloat16* wr = wsm + (nt * 8 + g) * kRgXRow + kk * 16 + 2 * tq;
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wr);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wr + 8);
+          mma_bf16_16816(acc[nt], a0, a1, a2, a3, b0, b1);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();   // ring idle: reuse it for the logits tile
+    constexpr int EP = NT * 8 + 1;
+    float* s_log = reinterpret_cast<float*>(rg_smem) + warp * 16 * EP;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const int c0 = nt * 8 + 2 * tq;
+      const float b0 = (bias && c0 < E) ? bias[c0] : 0.f;
+      const float b1 = (bias && c0 + 1 < E) ? bias[c0 + 1] : 0.f;
+      s_log[g * EP + c0] = acc[nt][0] + b0;
+      s_log[g * EP + c0 + 1] = acc[nt][1] + b1;
+      s_log[(g + 8) * EP + c0] = acc[nt][2] + b0;
+      s_log[(g + 8) * EP + c0 + 1] = acc[nt][3] + b1;
+    }
+    __syncwarp();
+    if (lane < 16) {
+      const long t = tok0 + warp * 16 + lane;
+      if (t < Tn)
+        finish_token(s_log + lane * EP, E, k, renorm, idx + t * k, w + t * k,
+                     probs ? probs + t * E : nullptr, s_hist);
+    }
+    __syncthreads();   // logits tile consumed before the ring is refilled
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x)
+    if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
+}
+
 }  // namespace lz
 
 using namespace lz;
@@ -368,6 +489,36 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
   const auto* xb = (const __nv_bfloat16*)x;
   const auto* wb = (const __nv_bfloat16*)wg;
   const int NT = (E + 7) / 8;
+  if (NT > 2 && d % kRgK == 0) {
+    // wide router: the block-shared pipelined kernel (persistent, 2 blocks per SM)
+    const int pgrid = grid < 2 * lzh::num_sms() ? grid : 2 * lzh::num_sms();
+#define LZ_ROUTER_PIPE(n)                                                                    \
+  case n: {                                                                                  \
+    static bool attr = false;                                                                \
+    if (!attr) {                                                                             \
+      if (cudaFuncSetAttribute(router_gate_pipe<n>,                                          \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
+                               RgCfg<n>::kSmem) != cudaSuccess)                              \
+        return lzh::check_launch();                                                          \
+      attr = true;                                                                           \
+    }                                                                                        \
+    router_gate_pipe<n><<<pgrid, 32 * kRouterWarps, RgCfg<n>::kSmem, s>>>(                   \
+        xb, wb, bias, Tn, d, E, k, renorm, idx, w, probs, hist);                             \
+    break;                                                                                   \
+  }
+    switch (NT) {
+      LZ_ROUTER_PIPE(3)
+      LZ_ROUTER_PIPE(4)
+      LZ_ROUTER_PIPE(5)
+      LZ_ROUTER_PIPE(6)
+      LZ_ROUTER_PIPE(7)
+      LZ_ROUTER_PIPE(8)
+      default:
+        return LZ_ERR_UNSUPPORTED;
+    }
+#undef LZ_ROUTER_PIPE
+    return lzh::check_launch();
+  }
 #define LZ_ROUTER_CASE(n)                                                                    \
   case n:                                                                                    \
     router_gate_kernel<n><<<grid, 32 * kRouterWarps, 0, s>>>(xb, wb, bias, Tn, d, E, k,       \
