@@ -174,6 +174,51 @@ __device__ __forceinline__ void tc_mma_cg(uint32_t tmem_d, uint64_t adesc, uint6
   }
 }
 
+// Warp-uniform issue: the whole MMA warp runs the issue loop (uniform control flow, so
+// descriptors and stage indices live in uniform registers) and elect.sync picks the one
+// lane that issues, inside the same asm block.  Issuing from `if (lane == 0)` instead
+// made ptxas wrap every tcgen05.mma in an ELECT / R2UR.BROADCAST / BRA.U.ANY waterfall
+// loop (~95 instructions per 64-deep k block), and with two heavy-epilogue warps on the
+// same SMSP the issuer fell behind the tensor pipe (ncu r01e: GELU GEMM 62 % active).
+template <int CG>
+__device__ __forceinline__ void tc_mma_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accum) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+  }
+}
+template <int CG>
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  if (CG == 1) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+            smem_u32(bar))
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 "
+        "[%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0,
                                              int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
@@ -765,9 +810,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ===== MMA issuer (leader CTA issues for the pair) =====
+    if (leader) {
+      // ===== MMA issuer (leader CTA issues for the pair; whole warp, one elected lane) ====
       constexpr uint32_t idesc = make_idesc(A_MN, B_MN, BM * CG);
+      // descriptors of stage 0; stage s / k step k are plain adds to the start-address
+      // field (smem addresses < 256 KB: (addr >> 4) never carries out of its 14 bits)
+      const uint32_t sa0 = smem_u32(s_tiles);
+      const uint64_t da0 = A_MN ? make_desc(sa0, 8192, 1024) : make_desc(sa0, 16, 1024);
+      const uint64_t db0 = B_MN ? make_desc(sa0 + C::kATileBytes, 8192, 1024)
+                                : make_desc(sa0 + C::kATileBytes, 16, 1024);
+      // K-major: +32 B per 16-element k step inside the 128 B swizzle atom
+      // MN-major: +2 x (8 rows x 128 B) per 16 k rows; atoms along MN are 8 KB apart
+      constexpr uint64_t kStepA = A_MN ? (2048 >> 4) : (32 >> 4);
+      constexpr uint64_t kStepB = B_MN ? (2048 >> 4) : (32 >> 4);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -781,25 +836,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < t.nk; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t sa = smem_u32(s_tiles + stage * C::kStageBytes);
-          const uint32_t sb = sa + C::kATileBytes;
+          const uint64_t soff = (uint64_t)(stage * (C::kStageBytes >> 4));
+          const uint64_t ad = da0 + soff, bd = db0 + soff;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major: +32 B per 16-element k step inside the 128 B swizzle atom
-            // MN-major: +2 x (8 rows x 128 B) per 16 k rows; atoms along MN are 8 KB apart
-            const uint64_t ad = A_MN ? make_desc(sa + k * 2048, 8192, 1024)
-                                     : make_desc(sa + k * 32, 16, 1024);
-            const uint64_t bd = B_MN ? make_desc(sb + k * 2048, 8192, 1024)
-                                     : make_desc(sb + k * 32, 16, 1024);
-            tc_mma_cg<CG>(d_tmem, ad, bd, idesc, (kb | k) != 0);
-          }
-          tc_commit_cg<CG>(&empty_bar[stage]);  // frees the smem slot(s) when the MMAs retire
+          for (int k = 0; k < BK / 16; ++k)
+            tc_mma_elect<CG>(d_tmem, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
+          tc_commit_elect<CG>(&empty_bar[stage]);  // frees the smem slot(s) when the MMAs retire
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit_cg<CG>(&tfull_bar[acc]);  // accumulator ready for the epilogue(s)
+        tc_commit_elect<CG>(&tfull_bar[acc]);  // accumulator ready for the epilogue(s)
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
