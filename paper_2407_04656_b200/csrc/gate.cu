@@ -447,6 +447,183 @@ __global__ void __launch_bounds__(32 * kRouterWarps, 2) router_gate_pipe(
     if (s_hist[e]) atomicAdd(&hist[e], s_hist[e]);
 }
 
+// ---------------------------------------------------------------------------
+// Streaming router for the common shape (E <= 16, d % 64 == 0, d <= 1024): one
+// persistent CTA per SM owns a CONTIGUOUS token range, so x streams from HBM in order.
+// Warp roles:
+//   producer (1 lane)  moves each 16-token group (16 rows of d * 2 bytes) into a 4-stage
+//                      shared-memory ring with cp.async.bulk (one copy per row into
+//                      16-byte-padded rows: conflict-free ldmatrix), completing on an
+//                      mbarrier;
+//   4 MMA warps        split the d columns (d / 4 each) and run mma.sync against Wg held
+//                      in shared memory; each writes its 16 x 16 partial logits to its
+//                      slot of one of 12 rotating tiles (tile_full: 4 arrivals);
+//   6 finisher warps   take the groups round-robin: sum the 4 slots in a fixed order
+//                      (deterministic and independent of the token's batch position)
+//                      + bias, softmax / top-k with one lane per token, then release the
+//                      tile (tile_empty).
+// The register-direct kernel below needs 2 waves of 16-token warps at 64K tokens, each
+// warp latency-bound on 4 KB in flight.
+// ---------------------------------------------------------------------------
+constexpr int kGsMma = 4;         // MMA (column-split) warps
+constexpr int kGsFin = 6;         // finisher warps
+constexpr int kGsStages = 4;      // x ring depth
+constexpr int kGsTiles = 12;      // partial-logit tiles
+constexpr int kGsEP = 17;         // padded partial row (16 experts + 1)
+constexpr int kGsThreads = 32 * (kGsMma + kGsFin + 1);
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void gs_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void gs_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+template <int NT>
+__global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
+    const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
+    const float* __restrict__ bias, int Tn, int d, int E, int k, int renorm,
+    int32_t* __restrict__ idx, float* __restrict__ w, float* __restrict__ probs,
+    int32_t* __restrict__ hist) {
+  extern __shared__ __align__(128) uint8_t gs_smem[];
+  __shared__ __align__(8) uint64_t full_bar[kGsStages], empty_bar[kGsStages];
+  __shared__ __align__(8) uint64_t tfull_bar[kGsTiles], tempty_bar[kGsTiles];
+  __shared__ int32_t s_hist[16];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int rowb = (d + 8) * 2;                    // padded smem row, bytes
+  uint8_t* ring = gs_smem;                         // [stages][16][d + 8] bf16
+  uint8_t* wsm = ring + kGsStages * 16 * rowb;     // [16][d + 8] bf16
+  float* part = reinterpret_cast<float*>(wsm + 16 * rowb);  // [tiles][kGsMma][16][kGsEP]
+  const int ng = (Tn + 15) / 16;
+  const int g_begin = (int)((long)ng * blockIdx.x / gridDim.x);
+  const int g_end = (int)((long)ng * (blockIdx.x + 1) / gridDim.x);
+  if (threadIdx.x < 16) s_hist[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kGsStages; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full_bar[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&empty_bar[i])),
+                   "r"(kGsMma));
+    }
+    for (int i = 0; i < kGsTiles; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&tfull_bar[i])),
+                   "r"(kGsMma));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&tempty_bar[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // router weights -> smem (rows >= E zero)
+  for (int q = threadIdx.x; q < 16 * (d / 8); q += blockDim.x) {
+    const int e = q / (d / 8), c = q % (d / 8);
+    const uint4 v = e < E ? ld_v4(wg + (long)e * d + c * 8) : make_uint4(0, 0, 0, 0);
+    *reinterpret_cast<uint4*>(wsm + e * rowb + c * 16) = v;
+  }
+  __syncthreads();
+  if (warp == kGsMma + kGsFin) {
+    // ===== producer: lane r issues row r's copy (16 bulk copies per instruction) =====
+    for (int gi = g_begin, i = 0; gi < g_end; ++gi, ++i) {
+      const int st = i % kGsStages;
+      if (i >= kGsStages) gs_wait(&empty_bar[st], ((i / kGsStages) - 1) & 1);
+      const long t0 = (long)gi * 16;
+      const int nv = (int)min(16L, (long)Tn - t0);
+      const uint32_t fb = smem_u32(&full_bar[st]);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                     "r"((uint32_t)(nv * d * 2))
+                     : "memory");
+      __syncwarp();
+      if (lane < nv)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(smem_u32(ring + st * 16 * rowb) + lane * rowb),
+            "l"(x + (t0 + lane) * d), "r"(d * 2), "r"(fb)
+            : "memory");
+    }
+  } else if (warp < kGsMma) {
+    // ===== MMA warps: columns [warp * d / 4, +d / 4) =====
+    const int g = lane >> 2, tq = lane & 3;
+    const int cw = d / kGsMma;
+    const int c_base = warp * cw;
+    for (int gi = g_begin, i = 0; gi < g_end; ++gi, ++i) {
+      const int st = i % kGsStages;
+      gs_wait(&full_bar[st], (i / kGsStages) & 1);
+      float acc[NT][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[nt][q] = 0.f;
+      const uint32_t sx = smem_u32(ring + st * 16 * rowb);
+#pragma unroll 4
+      for (int kk = 0; kk < cw; kk += 16) {
+        const int c = c_base + kk;
+        uint32_t a0, a1, a2, a3;
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                     : "r"(sx + (lane & 15) * rowb + (c + (lane >> 4) * 8) * 2));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const uint8_t* wr = wsm + (nt * 8 + g) * rowb + (c + 2 * tq) * 2;
+          const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wr);
+          const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wr + 16);
+          mma_bf16_16816(acc[nt], a0, a1, a2, a3, b0, b1);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) gs_arrive(&empty_bar[st]);
+      const int tile = i % kGsTiles;
+      if (i >= kGsTiles) gs_wait(&tempty_bar[tile], ((i / kGsTiles) - 1) & 1);
+      float* pw = part + ((tile * kGsMma + warp) * 16) * kGsEP;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int c0 = nt * 8 + 2 * tq;
+        pw[g * kGsEP + c0] = acc[nt][0];
+        pw[g * kGsEP + c0 + 1] = acc[nt][1];
+        pw[(g + 8) * kGsEP + c0] = acc[nt][2];
+        pw[(g + 8) * kGsEP + c0 + 1] = acc[nt][3];
+      }
+      __syncwarp();
+      if (lane == 0) gs_arrive(&tfull_bar[tile]);
+    }
+  } else {
+    // ===== finisher warps: groups f, f + kGsFin, ... =====
+    const int f = warp - kGsMma;
+    for (int i = f; g_begin + i < g_end; i += kGsFin) {
+      const int tile = i % kGsTiles;
+      gs_wait(&tfull_bar[tile], (i / kGsTiles) & 1);
+      const long t = (long)(g_begin + i) * 16 + lane;
+      if (lane < 16 && t < Tn) {
+        float* lg = part + ((tile * kGsMma) * 16 + lane) * kGsEP;  // MMA warp 0's slot
+        for (int e = 0; e < E; ++e) {
+          float v = lg[e];
+#pragma unroll
+          for (int ww = 1; ww < kGsMma; ++ww) v += lg[ww * 16 * kGsEP + e];
+          lg[e] = v + (bias ? __ldg(bias + e) : 0.f);
+        }
+        finish_token(lg, E, k, renorm, idx + t * k, w + t * k, probs ? probs + t * E : nullptr,
+                     s_hist);
+      }
+      __syncwarp();
+      if (lane == 0) gs_arrive(&tempty_bar[tile]);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < E && s_hist[threadIdx.x]) atomicAdd(&hist[threadIdx.x], s_hist[threadIdx.x]);
+}
+__host__ __device__ constexpr size_t gs_smem_bytes(int d) {
+  return (size_t)(kGsStages + 1) * 16 * (d + 8) * 2 +
+         (size_t)kGsTiles * kGsMma * 16 * kGsEP * sizeof(float);
+}
+
 }  // namespace lz
 
 using namespace lz;
@@ -489,6 +666,22 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
   const auto* xb = (const __nv_bfloat16*)x;
   const auto* wb = (const __nv_bfloat16*)wg;
   const int NT = (E + 7) / 8;
+  if (E <= 16 && d % 64 == 0 && d <= 1024) {
+    // streaming kernel: one persistent CTA per SM over a contiguous token range (for
+    // every Tn, so a token's logits never depend on the batch it came in)
+    const size_t smem = gs_smem_bytes(d);
+    const int ngroups = (Tn + 15) / 16;
+    const int sgrid = ngroups < lzh::num_sms() ? ngroups : lzh::num_sms();
+#define LZ_ROUTER_STREAM(n)                                                                    case n: {                                                                                      static bool attr = false;                                                                    if (!attr) {                                                                                   if (cudaFuncSetAttribute(router_gate_stream<n>,                                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,                                                 (int)gs_smem_bytes(1024)) != cudaSuccess)                             return lzh::check_launch();                                                                attr = true;                                                                               }                                                                                            router_gate_stream<n><<<sgrid, kGsThreads, smem, s>>>(xb, wb, bias, Tn, d, E, k,                                                                    renorm, idx, w, probs,                                                                       hist);                        break;                                                                                     }
+    switch (NT) {
+      LZ_ROUTER_STREAM(1)
+      LZ_ROUTER_STREAM(2)
+      default:
+        return LZ_ERR_UNSUPPORTED;
+    }
+#undef LZ_ROUTER_STREAM
+    return lzh::check_launch();
+  }
   if (NT > 2 && d % kRgK == 0) {
     // wide router: the block-shared pipelined kernel (persistent, 2 blocks per SM)
     const int pgrid = grid < 2 * lzh::num_sms() ? grid : 2 * lzh::num_sms();

@@ -41,7 +41,8 @@ def test_gate_topk_exact_ids(Tn, E, k, renorm):
 
 @pytest.mark.parametrize("Tn,d,E,k", [(4096, 1024, 16, 2), (1000, 512, 8, 2), (257, 2048, 64, 1),
                                       (100, 4096, 8, 2), (70000, 1024, 16, 2), (300, 96, 5, 1),
-                                      (513, 256, 40, 3)])
+                                      (513, 256, 40, 3), (2405, 512, 8, 1), (40000, 256, 16, 2),
+                                      (5003, 1024, 3, 1), (3000, 128, 12, 4)])
 def test_router_gate(Tn, d, E, k):
     g = torch.Generator().manual_seed(d)
     x = torch.randn(Tn, d, generator=g).bfloat16()
@@ -59,6 +60,13 @@ def test_router_gate(Tn, d, E, k):
     assert safe.float().mean() > 0.9
     assert torch.equal(idx.cpu()[safe], ridx[safe])
     assert int(hist.sum()) == Tn * k
+    assert torch.equal(hist.cpu(), torch.bincount(idx.cpu().reshape(-1).long(), minlength=E).int())
+    # a token's logits do not depend on its position in the batch (the streaming kernel
+    # splits the batch into per-SM ranges): any row subset routes identically
+    sub = torch.arange(Tn - 1, -1, -3)
+    idx2, w2, probs2, _ = ops.router_gate(x[sub].cuda(), wg.cuda(), bias.cuda(), k)
+    assert torch.equal(idx2.cpu(), idx.cpu()[sub])
+    assert torch.equal(probs2.cpu(), probs.cpu()[sub])
 
 
 def _rows(Tn, k, n_rows, gen):
