@@ -113,12 +113,14 @@ def test_combine_and_backward():
     del E
 
 
-@pytest.mark.parametrize("renorm", [False, True])
-def test_dispatch_bwd_and_router_grads(renorm):
+@pytest.mark.parametrize("renorm,Tn,d,E,k", [(False, 1024, 512, 16, 2), (True, 1024, 512, 16, 2),
+                                              (False, 5003, 1024, 8, 1), (True, 3001, 256, 12, 2),
+                                              (False, 700, 2048, 16, 2), (True, 257, 512, 32, 3)])
+def test_dispatch_bwd_and_router_grads(renorm, Tn, d, E, k):
     """dx = sum_s dxe[row] + dlogits . wg and dlogits from the softmax/top-k backward,
-    against torch autograd on the same fp32 math."""
+    against torch autograd on the same fp32 math (streaming kernel: E <= 16, k <= 2,
+    d % 256 == 0, d <= 1024; the register-prefetch kernel otherwise)."""
     gen = torch.Generator().manual_seed(7)
-    Tn, d, E, k = 1024, 512, 16, 2
     x = torch.randn(Tn, d, generator=gen).bfloat16()
     wg = (torch.randn(E, d, generator=gen) * 0.05).bfloat16()
     logits = (x.float() @ wg.float().t()).requires_grad_(True)
