@@ -181,7 +181,7 @@ def run_reference(args, cfg):
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -524,7 +524,7 @@ def run_gpu(args, cfg):
                                     "sample": f"{tok} tokens ({reps} x {ctok}) of the "
                                               f"same layer {'fwd+bwd' if cfg['bwd'] else 'fwd'} "
                                               f"on 1 rank, {dt:.1f} s"}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -629,7 +629,7 @@ def run_virtual(args, cfg):
                     "h2d_bytes_per_step": sum(h.numel() * 2 for h in host),
                     "d2h_bytes_per_step": 4},
             "gpu_launches": launches, "clocks": clocks, "cpu_baseline": cpu}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -736,7 +736,7 @@ def run_dispatch_sweep(args, cfg):
                          "frac": ref["pack_frac"], "combine_frac": ref["combine_frac"],
                          "peak_kind": f"{src} copy bandwidth", "traffic": None},
             "sweep": sweep}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -818,7 +818,7 @@ def run_elastic(args, cfg):
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
                 "config": {"workload": cfg["name"], "slots_per_gpu": c, "start_gpus": world},
                 "phases": phases, "reconfigurations": reconf}
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.barrier(group=group)
     dist.destroy_process_group()
     return 0
@@ -832,7 +832,22 @@ def plan_replicas(plan, E):
     return counts
 
 
+_OUT = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line on the real stdout (libraries' own chatter goes to stderr)."""
+    out = _OUT if _OUT is not None else sys.stdout
+    print(json.dumps(line), file=out, flush=True)
+
+
 def main():
+    global _OUT
+    # fd 1 -> stderr for everything else in the process (e.g. NCCL's version banner when
+    # NCCL_DEBUG is set on the box), so stdout carries exactly the JSON line
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
