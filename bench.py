@@ -28,17 +28,17 @@ sys.path.insert(0, ROOT)
 
 CONFIGS = {
     # name: E, k, d, d_ff, tokens per GPU, zipf s, slot factor (c = ceil(f*E/N)), bwd.
-    # slot_factor 5: with Zipf(1.2) top-2 loads the reference's MRO plans reach max/mean
-    # receive 1.13-1.14 at N = 4, 8 (factor 3: 1.49)
+    # slot_factor 6 (cfg2/cfg5): with Zipf(1.2) top-2 loads the reference's MRO plans reach
+    # max/mean receive 1.07 at N = 4 (factor 5: 1.15, 3: 1.49)
     "cfg1": dict(E=8, k=2, d=512, dff=2048, tokens=1024, s=1.2, slot_factor=2, bwd=False,
                  name="CPU-ref MoE layer (E8 top-2 d512 d_ff2048, 1024 tok/rank, fwd)"),
-    "cfg2": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=5, bwd=True,
+    "cfg2": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=6, bwd=True,
                  name="GPT-MoE layer (E16 top-2 d1024 d_ff4096, 64K tok/GPU, fwd+bwd)"),
     "cfg3": dict(E=8, k=2, d=4096, dff=14336, tokens=16384, s=1.2, slot_factor=5, bwd=True,
                  act="swiglu", cpu_tokens=256, cpu_reps=1,
                  name="Mixtral-8x7B-shape MoE layer (E8 top-2 d4096 d_ff14336 SwiGLU, 16K tok/GPU, "
                       "fwd+bwd + replica-group grad all-reduce)"),
-    "cfg5": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=5, bwd=True,
+    "cfg5": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=6, bwd=True,
                  name="elastic reconfiguration 8->6->4 (cfg2 shape, slots held at the 8-GPU value)"),
     "cfg4": dict(E=64, k=1, d=2048, dff=None, tokens=131072, s=1.5, slot_factor=4, bwd=False,
                  name="E64 top-1 d2048 dispatch/combine-only sweep (8K..1M tok/GPU, Zipf 1.5)"),
@@ -857,8 +857,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager steps only")
     ap.add_argument("--cpu-reps", type=int, default=12)
+    ap.add_argument("--slot-factor", type=float, default=None,
+                    help="slots per GPU = ceil(f * E / N) (default: the config's)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.slot_factor is not None:
+        cfg["slot_factor"] = args.slot_factor
     if args.impl == "reference":
         return run_reference(args, cfg)
     if args.config == "cfg4":
