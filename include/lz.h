@@ -116,7 +116,9 @@ lz_status lz_gate_topk(const float* logits, int Tn, int E, int k, int renorm, in
                        float* w, float* probs, int32_t* hist, void* stream);
 
 /* Fused router: logits = x[Tn, d] (bf16) . wg[E, d]^T (bf16) + bias[E] (fp32, may be
- * NULL), fp32 accumulate, then as lz_gate_topk.  d % 32 == 0, E <= 64. */
+ * NULL), fp32 accumulate, then as lz_gate_topk.  d % 32 == 0, E <= 64; x and wg
+ * 16-byte aligned (LZ_ERR_ARG otherwise).  A token's logits depend only on its row
+ * (fixed accumulation order for a given d, E), never on Tn or its position. */
 lz_status lz_router_gate(const void* x, const void* wg, const float* bias, int Tn, int d, int E,
                          int k, int renorm, int32_t* idx, float* w, float* probs, int32_t* hist,
                          void* stream);

@@ -662,6 +662,7 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
   if (cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess) return lzh::check_launch();
   if (Tn == 0) return LZ_OK;
   if (!x || !wg || !idx || !w) return LZ_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wg)) % 16) return LZ_ERR_ARG;
   const int grid = (Tn + kRouterTok - 1) / kRouterTok;
   const auto* xb = (const __nv_bfloat16*)x;
   const auto* wb = (const __nv_bfloat16*)wg;
