@@ -478,7 +478,7 @@ def run_gpu(args, cfg):
                     f"routing via router bias",
             "config": {"workload": cfg["name"], "experts": E, "top_k": k, "d_model": d,
                        "d_ff": dff, "tokens_per_gpu": Tn, "global_tokens": world * Tn,
-                       "slots_per_gpu": c, "fault_threshold": 2,
+                       "slots_per_gpu": c, "fault_threshold": 2, "zipf_s": cfg["s"],
                        "replicas": list(plan_replicas(plan, E)),
                        "imbalance_max_over_mean_recv": round(imbalance, 4),
                        "l2": "inputs larger than L2 (x alone 134 MB; step working set > 4 GB)",
@@ -859,8 +859,13 @@ def main():
     ap.add_argument("--cpu-reps", type=int, default=12)
     ap.add_argument("--slot-factor", type=float, default=None,
                     help="slots per GPU = ceil(f * E / N) (default: the config's)")
+    ap.add_argument("--zipf", type=float, default=None,
+                    help="Zipf exponent of the synthetic routing (default: the config's; "
+                         "2.5 = the paper-skew variant, top-2 share ~88 %% at E = 16)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    if args.zipf is not None:
+        cfg["s"] = args.zipf
     if args.slot_factor is not None:
         cfg["slot_factor"] = args.slot_factor
     if args.impl == "reference":
