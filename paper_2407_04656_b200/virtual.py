@@ -13,6 +13,8 @@ to back in one buffer).
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib, ops
@@ -63,6 +65,11 @@ class VirtualEP:
         self.Y = torch.empty_like(self.X)
         self._none = torch.empty(0, dtype=torch.int32, device=dev)
         self.last_plans = None
+        # the per-rank stages (gate, plan, pack, combine) are a few CTAs each: run the N
+        # virtual ranks' chains concurrently on N streams (fork / join; under graph capture
+        # they become parallel branches of the graph)
+        self.streams = ([torch.cuda.Stream(device=dev) for _ in range(self.N)]
+                        if os.environ.get("LZ_VIRTUAL_STREAMS", "1") != "0" else None)
         # scatter mode (the multi-GPU default): the second GEMM's epilogue writes every
         # output row straight back to its source rank's return buffer (row = assignment),
         # through the owner-side return map the dispatch records
@@ -74,14 +81,29 @@ class VirtualEP:
             self.ret_host = [self.YR[r].data_ptr() for r in range(self.N)]
             self.peers_ret = torch.tensor(self.ret_host, dtype=torch.int64, device=dev)
 
+    def _per_rank(self, fn):
+        """[fn(r) for r in ranks], rank r's launches on stream r (joined before return)."""
+        if self.streams is None:
+            return [fn(r) for r in range(self.N)]
+        main = torch.cuda.current_stream(self.device)
+        out = []
+        for r, st in enumerate(self.streams):
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                out.append(fn(r))
+        for st in self.streams:
+            main.wait_stream(st)
+        return out
+
     @torch.no_grad()
     def forward(self, xs):
         """xs: list of N [tokens_per_rank, d] bf16 tensors -> list of N outputs."""
         N, E, k, d, d_ff = self.N, self.E, self.k, self.d, self.d_ff
-        gates = [ops.router_gate(x, self.wg, self.bg, k, probs=False) for x in xs]
+        gates = self._per_rank(lambda r: ops.router_gate(xs[r], self.wg, self.bg, k, probs=False))
         T = torch.stack([gt[3] for gt in gates], dim=1).contiguous()   # all-gather analog
         align = ops.row_align()
-        plans = [plan_device(T, self.R_dev, r, gates[r][0].view(-1), align) for r in range(N)]
+        plans = self._per_rank(lambda r: plan_device(T, self.R_dev, r, gates[r][0].view(-1),
+                                                     align))
         self.last_plans = plans
         offs = torch.stack([p.recv_off for p in plans]).to(torch.int64)          # [N, E+1]
         base = torch.cumsum(offs[:, E], 0) - offs[:, E]                         # [N]
@@ -92,7 +114,7 @@ class VirtualEP:
         if self.scatter:
             ret_peers = base * 8 + self.RET.data_ptr()
             self.RET.fill_(-1)   # pad rows of every region
-        for r in range(N):   # every rank scatters its rows into the owners' regions
+        def pack(r):   # every rank scatters its rows into the owners' regions (disjoint)
             # forward only: pad rows are never read back, so they are not zeroed (E = 0)
             if self.scatter:
                 ops.pack_p2p_ret(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
@@ -100,6 +122,7 @@ class VirtualEP:
             else:
                 ops.pack_p2p(xs[r], plans[r].dest_rank, plans[r].dest_row, k, peers_x, self.X,
                              self._none, self._none)
+        self._per_rank(pack)
         swi = self.activation == "swiglu"
         H = torch.empty((self.cap, 2 * d_ff if swi else d_ff), dtype=torch.bfloat16,
                         device=self.device)
@@ -109,10 +132,11 @@ class VirtualEP:
         if self.scatter:
             ops.grouped_gemm_scatter(A, self.w2, off, self.Y, self.RET, self.peers_ret,
                                      self.ret_host, self.YR.shape[1])
-            return [ops.combine(self.YR[r], plans[r].slot, gates[r][1], k) for r in range(N)]
+            return self._per_rank(lambda r: ops.combine(self.YR[r], plans[r].slot, gates[r][1],
+                                                        k))
         ops.grouped_gemm_rows(A, self.w2, off, self.Y)
-        return [ops.combine_p2p(peers_y, plans[r].dest_rank, plans[r].dest_row, gates[r][1],
-                                k, d) for r in range(N)]
+        return self._per_rank(lambda r: ops.combine_p2p(peers_y, plans[r].dest_rank,
+                                                        plans[r].dest_row, gates[r][1], k, d))
 
     __call__ = forward
 
