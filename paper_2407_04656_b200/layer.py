@@ -138,6 +138,7 @@ class MoELayer(torch.nn.Module):
         self.local_ids = [e for e in range(self.E) if R[e][self.rank] > 0]
         ext = self.local_ids + [self.E]
         self._off_index = torch.tensor(ext, dtype=torch.long, device=self.device)
+        self._all_local = len(self.local_ids) == self.E   # off = recv_off (no gather launch)
         w1s, w2s = [], []
         for e in self.local_ids:
             if weights is not None and e in weights:
@@ -242,7 +243,8 @@ class _MoEFunction(torch.autograd.Function):
         _mark(layer, "hist_allgather")
         plan = plan_device(T, layer.R_dev, rank, idx.view(-1), ops.row_align())
         layer.last_plan = plan
-        off = plan.recv_off.index_select(0, layer._off_index).contiguous()
+        off = plan.recv_off.contiguous() if layer._all_local else \
+            plan.recv_off.index_select(0, layer._off_index).contiguous()
         _mark(layer, "plan")
         P = Tn * k
         sizes = None
