@@ -52,3 +52,4 @@ t(lambda: ops.dispatch_bwd(dxe, seq_rows, probs, idx, dw, None, False, Tn),
   "dispatch_bwd (no router term, sequential rows)", P * d * 2 + Tn * d * 2 + 2 * Tn * E * 4)
 t(lambda: ops.combine_bwd(dout, y, seq_rows, w, k, dy), "combine_bwd (sequential rows)",
   Tn * d * 2 + 2 * P * d * 2 + P * 8)
+t(lambda: ops.router_wgrad(logits, dout), "router_wgrad", Tn * d * 2 + Tn * E * 4)
