@@ -522,32 +522,52 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  // router weights -> smem (rows >= E zero)
-  for (int q = threadIdx.x; q < 16 * (d / 8); q += blockDim.x) {
-    const int e = q / (d / 8), c = q % (d / 8);
-    const uint4 v = e < E ? ld_v4(wg + (long)e * d + c * 8) : make_uint4(0, 0, 0, 0);
-    *reinterpret_cast<uint4*>(wsm + e * rowb + c * 16) = v;
+  __syncthreads();
+  // producer: lane r issues row r's copy of a 16-token group (16 bulk copies per instruction)
+  auto issue = [&](int gi, int i) {
+    const int st = i % kGsStages;
+    const long t0 = (long)gi * 16;
+    const int nv = (int)min(16L, (long)Tn - t0);
+    const uint32_t fb = smem_u32(&full_bar[st]);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                   "r"((uint32_t)(nv * d * 2))
+                   : "memory");
+    __syncwarp();
+    if (lane < nv)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+          "[%3];" ::"r"(smem_u32(ring + st * 16 * rowb) + lane * rowb),
+          "l"(x + (t0 + lane) * d), "r"(d * 2), "r"(fb)
+          : "memory");
+  };
+  const bool producer = warp == kGsMma + kGsFin;
+  // the first ring stages are in flight before the router weights are staged
+  if (producer)
+    for (int i = 0; i < kGsStages && g_begin + i < g_end; ++i) issue(g_begin + i, i);
+  {
+    // router weights -> smem (rows >= E zero), every thread's loads in flight at once
+    constexpr int kPer = (16 * 1024 / 8 + kGsThreads - 1) / kGsThreads;   // d <= 1024
+    const int nq = 16 * (d / 8);
+    uint4 v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int q = threadIdx.x + j * kGsThreads;
+      const int e = q / (d / 8), c = q % (d / 8);
+      v[j] = (q < nq && e < E) ? ld_v4(wg + (long)e * d + c * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int q = threadIdx.x + j * kGsThreads;
+      if (q < nq)
+        *reinterpret_cast<uint4*>(wsm + (q / (d / 8)) * rowb + (q % (d / 8)) * 16) = v[j];
+    }
   }
   __syncthreads();
-  if (warp == kGsMma + kGsFin) {
-    // ===== producer: lane r issues row r's copy (16 bulk copies per instruction) =====
-    for (int gi = g_begin, i = 0; gi < g_end; ++gi, ++i) {
-      const int st = i % kGsStages;
-      if (i >= kGsStages) gs_wait(&empty_bar[st], ((i / kGsStages) - 1) & 1);
-      const long t0 = (long)gi * 16;
-      const int nv = (int)min(16L, (long)Tn - t0);
-      const uint32_t fb = smem_u32(&full_bar[st]);
-      if (lane == 0)
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                     "r"((uint32_t)(nv * d * 2))
-                     : "memory");
-      __syncwarp();
-      if (lane < nv)
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-            "[%3];" ::"r"(smem_u32(ring + st * 16 * rowb) + lane * rowb),
-            "l"(x + (t0 + lane) * d), "r"(d * 2), "r"(fb)
-            : "memory");
+  if (producer) {
+    for (int gi = g_begin + kGsStages, i = kGsStages; gi < g_end; ++gi, ++i) {
+      gs_wait(&empty_bar[i % kGsStages], ((i / kGsStages) - 1) & 1);
+      issue(gi, i);
     }
   } else if (warp < kGsMma) {
     // ===== MMA warps: columns [warp * d / 4, +d / 4) =====
