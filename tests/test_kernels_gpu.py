@@ -42,7 +42,8 @@ def test_gate_topk_exact_ids(Tn, E, k, renorm):
 @pytest.mark.parametrize("Tn,d,E,k", [(4096, 1024, 16, 2), (1000, 512, 8, 2), (257, 2048, 64, 1),
                                       (100, 4096, 8, 2), (70000, 1024, 16, 2), (300, 96, 5, 1),
                                       (513, 256, 40, 3), (2405, 512, 8, 1), (40000, 256, 16, 2),
-                                      (5003, 1024, 3, 1), (3000, 128, 12, 4)])
+                                      (5003, 1024, 3, 1), (3000, 128, 12, 4), (5, 512, 16, 2),
+                                      (2368, 1024, 16, 2), (9472, 1024, 16, 2)])
 def test_router_gate(Tn, d, E, k):
     g = torch.Generator().manual_seed(d)
     x = torch.randn(Tn, d, generator=g).bfloat16()
