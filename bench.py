@@ -440,6 +440,11 @@ def run_gpu(args, cfg):
             "dispatch_bwd": Pa * d * 2 + Tn * d * 2 + 2 * Tn * E * 4,
             "router_wgrad": Tn * d * 2 + Tn * E * 4,
         }
+        if getattr(layer, "tail_overlap", False) and world == 1 and cfg["bwd"]:
+            # these two run on a side stream under the weight-gradient GEMMs: their time
+            # is inside `ffn_bwd` (isolated numbers: hbm_kernels)
+            stage_bytes.pop("dispatch_bwd")
+            stage_bytes.pop("router_wgrad")
         hbm_stages = {}
         if world == 1:
             for st_name, nbytes in stage_bytes.items():
@@ -507,6 +512,9 @@ def run_gpu(args, cfg):
             "stages_ms_rank0": stages,
             "hbm_stages": hbm_stages or None,
             "hbm_kernels": hbm_kernels,
+            "hbm_note": "hbm_stages: eager pass, a stage's events include host launch gaps "
+                        "(lower bounds); hbm_kernels: each kernel alone, 20 launches back to "
+                        "back on the step's shapes and routing",
             "stages_ms_per_rank": stages_all if world > 1 else None,
             "nvlink": None if nvlink is None else {
                 "per_rank": [{k2: round(v, 2) for k2, v in r.items()} for r in nvlink],
