@@ -105,17 +105,28 @@ __device__ void scan_block_counts(const int32_t* blk_counts, int32_t* blk_base, 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nwarps = blockDim.x / 32;
   for (int e = warp; e < E; e += nwarps) {
     int32_t carry = 0;
-    for (int b0 = 0; b0 < B; b0 += 32) {
-      int b = b0 + lane;
-      int32_t v = (b < B) ? blk_counts[e * B + b] : 0;
-      int32_t incl = v;
+    for (int b00 = 0; b00 < B; b00 += 32 * 8) {
+      int32_t vv[8];   // up to 8 chunks of 32 block counts in flight before the scans
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int32_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
+      for (int u = 0; u < 8; ++u) {
+        const int b = b00 + u * 32 + lane;
+        vv[u] = (b < B) ? blk_counts[e * B + b] : 0;
       }
-      if (b < B) blk_base[e * B + b] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int b0 = b00 + u * 32;
+        if (b0 >= B) break;
+        const int b = b0 + lane;
+        const int32_t v = vv[u];
+        int32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          int32_t w = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += w;
+        }
+        if (b < B) blk_base[e * B + b] = carry + incl - v;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
     }
     if (lane == 0 && carry != expect[e * stride]) atomicOr(err, LZ_ERRF_COUNTS);
   }
@@ -141,23 +152,40 @@ struct PlanArgs {
   int32_t* tab_pref;          // [E][N+1]  prefix of D[rank][e][:]
   int32_t* tab_sdelta;        // [E][N]    slot = m + sdelta
   int32_t* tab_ddelta;        // [E][N]    dest row = m + ddelta
+  int d_smem;                 // T, R and D staged in shared memory (they fit)
 };
 
 // Single block.  Dynamic smem: int64 q[E] | int32 M[N][E] | int32 padoff[N][E+1]
+// (+ int32 T[E][N] | R[E][N] | D[N][E][N] when d_smem: every later phase reads D from
+// shared memory instead of re-reading its own global writes)
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char s_raw[];
   const int E = a.E, N = a.N, rank = a.rank;
   int64_t* s_q = reinterpret_cast<int64_t*>(s_raw);
   int32_t* s_M = reinterpret_cast<int32_t*>(s_q + E);  // M[j][e] = sum_i D[i][e][j]
   int32_t* s_pad = s_M + N * E;                         // padoff[j][e], e in [0, E]
+  int32_t* s_T = s_pad + N * (E + 1);
+  int32_t* s_R = s_T + E * N;
+  int32_t* s_D = s_R + E * N;
   const int tid = threadIdx.x;
+  const int32_t* Tm = a.T;
+  const int32_t* Rm = a.R;
+  if (a.d_smem) {
+    for (int x = tid; x < E * N; x += blockDim.x) {
+      s_T[x] = a.T[x];
+      s_R[x] = a.R[x];
+    }
+    __syncthreads();
+    Tm = s_T;
+    Rm = s_R;
+  }
 
   // -- quotas (dispatch.py:143-151) -----------------------------------------
   for (int e = tid; e < E; e += blockDim.x) {
     int64_t t_e = 0, r_e = 0;
     for (int j = 0; j < N; ++j) {
-      t_e += a.T[e * N + j];
-      r_e += a.R[e * N + j];
+      t_e += Tm[e * N + j];
+      r_e += Rm[e * N + j];
     }
     int64_t q = 0;
     if (r_e > 0) q = (t_e + r_e - 1) / r_e;  // == ceil(float(t)/float(r)) for t < 2^52
@@ -170,11 +198,14 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   // -- all senders' rows (dispatch.py:152-159) --------------------------------
   for (int row = tid; row < N * E; row += blockDim.x) {
     const int i = row / E, e = row % E;
-    dispatch_row(i, N, a.T + e * N, a.R + e * N, s_q[e], a.D + (size_t)row * N);
+    dispatch_row(i, N, Tm + e * N, Rm + e * N, s_q[e],
+                 (a.d_smem ? s_D : a.D) + (size_t)row * N);
   }
   __syncthreads();
+  if (a.d_smem)
+    for (int x = tid; x < N * E * N; x += blockDim.x) a.D[x] = s_D[x];
 
-  const int32_t* D = a.D;
+  const int32_t* D = a.d_smem ? s_D : a.D;
   auto Dat = [&](int i, int e, int j) { return D[((size_t)i * E + e) * N + j]; };
 
   // -- per-destination received counts and padded expert-major offsets -----------
@@ -323,9 +354,11 @@ static lz_status check_EN(int E, int N) {
   return LZ_OK;
 }
 
-static size_t plan_smem(int E, int N) {
-  return sizeof(int64_t) * E + sizeof(int32_t) * (size_t)N * E + sizeof(int32_t) * (size_t)N * (E + 1);
+static size_t plan_smem(int E, int N, bool d_smem = false) {
+  return sizeof(int64_t) * E + sizeof(int32_t) * (size_t)N * E + sizeof(int32_t) * (size_t)N * (E + 1) +
+         (d_smem ? sizeof(int32_t) * ((size_t)2 * E * N + (size_t)N * E * N) : 0);
 }
+static bool plan_d_smem(int E, int N) { return plan_smem(E, N, true) <= 48 * 1024; }
 
 extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E, int N, int rank,
                                       const int32_t* routed, int P, int align, int64_t* quota,
@@ -362,8 +395,8 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
   }
   PlanArgs a{T, R, E, N, rank, align, P, B, quota, D, send_sizes, recv_sizes, recv_counts,
              recv_m, recv_off, recv_src_off, recv_stage_off, recv_cnt, err, blk_counts,
-             blk_base, pref, sdelta, ddelta};
-  const size_t smem = plan_smem(E, N);
+             blk_base, pref, sdelta, ddelta, plan_d_smem(E, N) ? 1 : 0};
+  const size_t smem = plan_smem(E, N, a.d_smem != 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   plan_kernel<<<1, kPlanThreads, smem, s>>>(a);
