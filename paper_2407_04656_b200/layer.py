@@ -416,6 +416,7 @@ class _MoEFunction(torch.autograd.Function):
             with torch.cuda.stream(side):
                 dx, dlog = ops.dispatch_bwd(dX, row, probs, idx, dw, wg, layer.renorm, Tn)
                 dwg, dbg = ops.router_wgrad(dlog, x)
+                dwg = dwg.to(wg.dtype)
             ops.grouped_gemm_wgrad(dH, X, off, dW1)
             ops.grouped_gemm_wgrad(dY, A, off, dW2)
             main.wait_stream(side)
@@ -426,7 +427,7 @@ class _MoEFunction(torch.autograd.Function):
             _mark(layer, "dispatch_bwd")
             _mark(layer, "router_wgrad")
             _mark(layer, "grad_sync")
-            return dx, dwg.to(wg.dtype), dbg, dW1, dW2, None
+            return dx, dwg, dbg, dW1, dW2, None
         if G > 0:
             # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H); on N > 1 the
             # tiles of our own rows start while the other ranks' dY rows arrive
