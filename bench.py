@@ -356,6 +356,9 @@ def run_gpu(args, cfg):
     layer.stage_events = []
     nb = 3
     for _ in range(nb):
+        # ~1 ms of device spin first: the host enqueues the step's first kernels while the
+        # GPU is still busy, so the stage events time the kernels, not host launch latency
+        torch.cuda._sleep(1 << 21)
         step(x, dout)
     torch.cuda.synchronize()
     stages = {k2: round(v / nb, 4) for k2, v in stage_breakdown(layer.stage_events).items()}
@@ -512,9 +515,10 @@ def run_gpu(args, cfg):
             "stages_ms_rank0": stages,
             "hbm_stages": hbm_stages or None,
             "hbm_kernels": hbm_kernels,
-            "hbm_note": "hbm_stages: eager pass, a stage's events include host launch gaps "
-                        "(lower bounds); hbm_kernels: each kernel alone, 20 launches back to "
-                        "back on the step's shapes and routing",
+            "hbm_note": "hbm_stages: eager pass behind a device spin (the GPU trails the "
+                        "host), events between stages, so they include inter-kernel gaps "
+                        "and small torch ops (lower bounds); hbm_kernels: each kernel alone, "
+                        "20 launches back to back on the step's shapes and routing",
             "stages_ms_per_rank": stages_all if world > 1 else None,
             "nvlink": None if nvlink is None else {
                 "per_rank": [{k2: round(v, 2) for k2, v in r.items()} for r in nvlink],
