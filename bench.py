@@ -325,7 +325,7 @@ def run_gpu(args, cfg):
                 pa.copy_(pb)
         # N > 1: keep the already rendezvoused symmetric buffers (no second collective
         # allocation, and the old ones are never freed under a rank's feet)
-        fresh._symm, fresh._symm_group = layer._symm, layer._symm_group
+        fresh._symm, fresh._rows_wanted = layer._symm, layer._rows_wanted
         layer = fresh
         for _ in range(3):
             step(x, dout)

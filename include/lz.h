@@ -44,12 +44,36 @@ typedef enum {
 #define LZ_ERRF_UNROUTABLE 1  /* t_e > 0 and r_e == 0          dispatch.py:147-150 */
 #define LZ_ERRF_COUNTS 2      /* routed list disagrees with T  dispatch.py:213-229 */
 #define LZ_ERRF_EXPERT_ID 4   /* routed expert id out of range dispatch.py:220-222 */
+#define LZ_ERRF_CAPACITY 8    /* a rank's padded receive rows (or a sender's assignments)
+                                 exceed the receive buffer: nothing was exchanged; the host
+                                 grows the buffers and re-runs the step                  */
 
 /* compiled limits */
 #define LZ_MAX_RANKS 64
 #define LZ_MAX_EXPERTS 1024
 #define LZ_MAX_EN 4096 /* E*N */
 #define LZ_MAX_TOPK 8
+
+/* Watchdog / abort control block (process-wide; on a failure the enqueued
+ * cross-rank waits time out and the step is discarded).  Every cross-rank wait of the
+ * library (arrival flags of lz_grouped_gemm_arrival, lz_peer_barrier) gives up after
+ * timeout_ns or as soon as the host raises `abort`, records why, and lets its kernel run
+ * to completion on whatever data is present -- no kernel hangs and none traps; the host
+ * discards the step.  Intra-kernel pipeline waits (a library bug, never a peer) record
+ * `watchdog` after ~10 s and give up likewise.  Place the block in mapped pinned host
+ * memory so the host can raise `abort` while kernels spin and poll the flags without a
+ * device synchronisation.  Without a block (NULL) cross-rank waits are bounded by 10 s
+ * and a stuck pipeline traps. */
+typedef struct lz_ctl {
+  int32_t abort;      /* host: non-zero -> every cross-rank wait gives up now            */
+  int32_t timeout;    /* device: set to 1 when a cross-rank wait exceeded timeout_ns      */
+  int32_t aborted;    /* device: set to 1 when a wait gave up because abort was raised    */
+  int32_t watchdog;   /* device: set to 1 when an intra-kernel pipeline wait hit ~10 s    */
+  int64_t timeout_ns; /* cross-rank wait budget (0: 10 s)                                 */
+  int64_t reserved;
+} lz_ctl;
+/* Install (or with NULL remove) the control block; synchronous, call outside capture. */
+lz_status lz_set_control(lz_ctl* ctl);
 
 const char* lz_status_string(int status);
 int lz_version(void);
@@ -83,9 +107,15 @@ lz_status lz_plan_workspace_bytes(int E, int N, int P, size_t* bytes);
  *   recv_stage_off[E*N], recv_cnt[E*N] (optional, both or neither): where the
  *             (source i, expert e) segment sits in a plain all-to-all receive buffer
  *             (source-major, expert-major inside) and its length D[i][e][rank]
- * `routed` may be NULL (P = 0) to compute counts only.  Errors -> `err`. */
+ * `routed` may be NULL (P = 0) to compute counts only.  Errors -> `err`.
+ * cap_rows > 0: rows of every rank's exchange buffers.  When any rank's padded receive
+ * rows or any sender's assignments exceed it, LZ_ERRF_CAPACITY is raised on EVERY rank
+ * (all evaluate the same plan), the receive layout is empty and every assignment stays
+ * local at row p % cap_rows -- the step runs harmlessly and the host grows the buffers to
+ * *need_rows (optional output: the largest of those row counts) and re-runs it. */
 lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E, int N, int rank,
-                           const int32_t* routed, int P, int align, int64_t* quota, int32_t* D,
+                           const int32_t* routed, int P, int align, int cap_rows,
+                           int32_t* need_rows, int64_t* quota, int32_t* D,
                            int32_t* send_sizes, int32_t* recv_sizes, int32_t* recv_counts,
                            int32_t* slot, int32_t* gather, int32_t* dest_row, int32_t* dest_rank,
                            int32_t* recv_m, int32_t* recv_off, int32_t* recv_src_off,
@@ -262,9 +292,6 @@ lz_status lz_grouped_gemm_scatter(const void* A, const void* B, void* C, int G,
                                   const unsigned long long* ret_peers,
                                   const unsigned long long* ret_peers_host, int n_peers,
                                   int ret_rows, void* stream);
-/* Retained for ABI compatibility: the register -> global epilogue variants were measured
- * 1.6-2x slower and removed; every call returns 0 (smem staging + TMA stores). */
-int lz_gemm_set_direct_epilogue(int on);
 /* Row alignment mode-0 group segments must have for the active variant (128 or 256). */
 int lz_gemm_row_align(void);
 
@@ -287,6 +314,13 @@ lz_status lz_epoch_bump(int* epoch, void* stream);
  * the n ranks' flag arrays (symmetric int32 [n]). */
 lz_status lz_signal_peers(const unsigned long long* flag_peers, int n, int my_rank,
                           const int* epoch, void* stream);
+/* Device-side cross-rank barrier on the stream (replaces the symmetric-memory barrier
+ * between the exchange's remote writes and the reads that depend on them): ++*counter,
+ * then flag_peers[j][my_rank] = *counter for every j < n (system fence + release store),
+ * then wait until own_flags[i] >= *counter for every i < n (acquire).  Bounded by the
+ * control block (lz_set_control): on timeout / abort it records the cause and returns. */
+lz_status lz_peer_barrier(const unsigned long long* flag_peers, int n, int my_rank, int* counter,
+                          const int* own_flags, void* stream);
 /* Arrival-ordered mode-0 grouped GEMM (the first expert GEMM of each direction on N > 1):
  * as lz_grouped_gemm(mode 0), but the tiles lying entirely inside self_rows[2g] ..
  * self_rows[2g+1] (the rows this rank dispatched to itself) run first, and the producer

@@ -21,7 +21,10 @@ _SIGS = {
     "lz_plan_workspace_bytes": [_i, _i, _i, ctypes.POINTER(ctypes.c_size_t)],
     # T R E N rank routed P align | quota D send recv recv_counts slot gather dest_row
     # dest_rank recv_m recv_off recv_src_off recv_stage_off recv_cnt err ws | ws_bytes stream
-    "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i] + [_vp] * 16 + [_sz, _vp],
+    # ... align cap_rows need_rows | quota ...
+    "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i, _i] + [_vp] * 17 + [_sz, _vp],
+    "lz_set_control": [_vp],
+    "lz_peer_barrier": [_vp, _i, _i, _vp, _vp, _vp],
     "lz_pack_p2p": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp],
     "lz_combine_p2p": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp],
     "lz_combine_bwd_p2p": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
@@ -52,14 +55,13 @@ _SIGS = {
     "lz_router_wgrad": [_vp, _vp, _i, _i, _i, _vp, _vp, _vp, _sz, _vp],
     "lz_gemm_set_cta_group": [_i],
     "lz_gemm_row_align": [],
-    "lz_gemm_set_direct_epilogue": [_i],
     "lz_grouped_gemm": [_i, _vp, _vp, _vp, _vp, _i, _vp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _vp],
 }
 _RESTYPE = {"lz_status_string": ctypes.c_char_p, "lz_router_wgrad_ws_bytes": ctypes.c_size_t}
 
 # header constants (include/lz.h)
 LZ_OK, LZ_ERR_ARG, LZ_ERR_UNROUTABLE, LZ_ERR_CUDA, LZ_ERR_WORKSPACE, LZ_ERR_UNSUPPORTED = range(6)
-LZ_ERRF_UNROUTABLE, LZ_ERRF_COUNTS, LZ_ERRF_EXPERT_ID = 1, 2, 4
+LZ_ERRF_UNROUTABLE, LZ_ERRF_COUNTS, LZ_ERRF_EXPERT_ID, LZ_ERRF_CAPACITY = 1, 2, 4, 8
 LZ_EPI_STORE, LZ_EPI_GELU, LZ_EPI_DGELU, LZ_EPI_SWIGLU, LZ_EPI_DSWIGLU = 0, 1, 2, 3, 4
 LZ_K_MAJOR, LZ_MN_MAJOR = 0, 1
 LZ_MAX_RANKS, LZ_MAX_EXPERTS, LZ_MAX_EN, LZ_MAX_TOPK = 64, 1024, 4096, 8
@@ -107,7 +109,7 @@ _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
             "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1, "lz_load_record": 1,
             "lz_recovery_count": 1, "lz_pack_p2p_ret": 1, "lz_combine_bwd_p2p_ret": 1,
             "lz_grouped_gemm_scatter": 1, "lz_epoch_bump": 1, "lz_signal_peers": 1,
-            "lz_grouped_gemm_arrival": 1}
+            "lz_grouped_gemm_arrival": 1, "lz_peer_barrier": 1}
 launch_count = 0
 
 
@@ -140,3 +142,50 @@ def stream_ptr(stream=None) -> int:
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return s.cuda_stream
+
+
+# ------------------------------------------------------------ watchdog control block
+
+class Ctl(ctypes.Structure):
+    """include/lz.h lz_ctl, in mapped pinned host memory (the host raises ``abort`` and
+    reads the device-set causes without a device synchronisation)."""
+    _fields_ = [("abort", ctypes.c_int32), ("timeout", ctypes.c_int32),
+                ("aborted", ctypes.c_int32), ("watchdog", ctypes.c_int32),
+                ("timeout_ns", ctypes.c_int64), ("reserved", ctypes.c_int64)]
+
+
+_ctl_tensor = None
+_ctl = None
+
+
+def control(timeout_s: float | None = None) -> Ctl:
+    """The process's control block (installed on first use; ``timeout_s`` sets the
+    cross-rank wait budget, default 10 s).  Host-visible view over pinned memory the
+    device reads and writes with system-scope accesses."""
+    global _ctl_tensor, _ctl
+    import torch
+    if _ctl is None:
+        t = torch.zeros(ctypes.sizeof(Ctl), dtype=torch.uint8).pin_memory()
+        _ctl_tensor = t
+        _ctl = Ctl.from_address(t.data_ptr())
+        call("lz_set_control", ctypes.c_void_p(t.data_ptr()))
+    if timeout_s is not None:
+        _ctl.timeout_ns = int(timeout_s * 1e9)
+    return _ctl
+
+
+def control_status() -> dict:
+    """Causes recorded by the device since the last :func:`control_reset` (no sync)."""
+    c = control()
+    return {"timeout": bool(c.timeout), "aborted": bool(c.aborted),
+            "watchdog": bool(c.watchdog), "abort_raised": bool(c.abort)}
+
+
+def control_abort() -> None:
+    """Make every cross-rank wait in flight (and every later one) give up now."""
+    control().abort = 1
+
+
+def control_reset() -> None:
+    c = control()
+    c.abort = c.timeout = c.aborted = c.watchdog = 0

@@ -50,7 +50,11 @@ class SymmetricRows:
     (torch symmetric memory: cuMem + IPC handles, one mapping per peer).  ``peers(b)``
     is a device int64 [N] array of every rank's address of buffer b, consumed by the
     fused P2P dispatch/combine kernels; ``barrier()`` is a device-side cross-rank
-    barrier on the current stream (orders P2P writes before the peers read)."""
+    barrier on the current stream (orders P2P writes before the peers read; bounded by
+    the watchdog control block, ``_lib.control``).
+
+    Collective: every rank must construct it with the same ``rows`` (``ProcessFabric``
+    agrees on the maximum first)."""
 
     def __init__(self, group, nbuf: int, rows: int, d: int, device):
         import torch.distributed._symmetric_memory as symm
@@ -74,15 +78,18 @@ class SymmetricRows:
         self.ret_ptrs = torch.tensor(
             [self.hr.get_remote_tensor(r, (rows,), torch.int64).data_ptr() for r in range(n)],
             dtype=torch.int64, device=device)
-        # arrival flags [2 (dispatch, combine-backward), n senders] + this rank's step epoch
+        # flags [3 (dispatch arrivals, combine-backward arrivals, barrier), n senders], this
+        # rank's step epoch and barrier count
         self.n = n
-        self.flags = symm.empty((2, n), dtype=torch.int32, device=device)
+        self.rank = self.h.rank
+        self.flags = symm.empty((3, n), dtype=torch.int32, device=device)
         self.flags.zero_()
         self.hf = symm.rendezvous(self.flags, group)
-        fb = [self.hf.get_remote_tensor(r, (2, n), torch.int32).data_ptr() for r in range(n)]
-        self.flag_peers = torch.tensor([[b + i * n * 4 for b in fb] for i in range(2)],
+        fb = [self.hf.get_remote_tensor(r, (3, n), torch.int32).data_ptr() for r in range(n)]
+        self.flag_peers = torch.tensor([[b + i * n * 4 for b in fb] for i in range(3)],
                                        dtype=torch.int64, device=device)
         self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        self.bar_count = torch.zeros(1, dtype=torch.int32, device=device)
         torch.cuda.synchronize(device)
         self.hf.barrier(channel=0)   # every rank's flags are zero before anyone signals
 
@@ -95,8 +102,10 @@ class SymmetricRows:
     def peers_host(self, i: int) -> list[int]:
         return self.host_ptrs[i]
 
-    def barrier(self) -> None:
-        self.h.barrier(channel=0)
+    def barrier(self, stream=None) -> None:
+        from . import ops
+        ops.peer_barrier(self.flag_peers[2], self.n, self.rank, self.bar_count, self.flags[2],
+                         stream)
 
 
 def owner_sets(R: Sequence[Sequence[int]]) -> list[tuple[int, ...]]:
@@ -178,3 +187,68 @@ class ReplicaGroups:
                 for a, b in runs:
                     works.append(dist.all_reduce(g[a:b], group=pg, async_op=True))
         return works
+
+
+# ---------------------------------------------------------------- exchange fabric
+
+# Requests a rank's layer step yields wherever ranks interact (layer._forward_steps /
+# _backward_steps).  A fabric serves them: ProcessFabric for one process per GPU
+# (NCCL + NVLink symmetric memory), loopback.LoopbackWorld for N ranks on one GPU.
+HIST = "hist"            # (hist [E] int32)                 -> T [E, N]
+SYNC = "sync"            # ()  every rank's launches so far precede what follows
+BARRIER = "barrier"      # (sym, stream)  device barrier over the exchange buffers
+SYMM = "symm"            # (rows, nbuf, d)                  -> exchange buffers
+EXPERT_AR = "expert_ar"  # (layer, grads)  replica-group sum  -> pending works
+WAIT = "wait"            # (works)
+ALLREDUCE = "allreduce"  # (flat tensor)  in-place sum over all ranks
+A2A = "a2a"              # (out, inp, out_splits, in_splits)  row all-to-all-v
+
+
+class ProcessFabric:
+    """One rank per process (the product path): serves the layer's requests with
+    torch.distributed (NCCL) collectives and the NVLink symmetric-memory buffers."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank, self.world = world(group)
+
+    def replica_groups(self, R, max_ctas=None):
+        return ReplicaGroups(R, self.group, max_ctas=max_ctas) if self.world > 1 else None
+
+    def run(self, gen):
+        """Drive one rank's step generator to completion; returns its value."""
+        res = None
+        while True:
+            try:
+                req = gen.send(res)
+            except StopIteration as stop:
+                return stop.value
+            res = self.serve(req)
+
+    def serve(self, req):
+        kind = req[0]
+        if kind == HIST:
+            return allgather_hist(req[1], self.group)
+        if kind == SYNC:
+            return None
+        if kind == BARRIER:
+            req[1].barrier(req[2])
+            return None
+        if kind == SYMM:
+            rows, nbuf, d, device = req[1:]
+            t = torch.tensor([rows], dtype=torch.int64, device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)   # ranks agree
+            return SymmetricRows(self.group, nbuf, int(t.item()), d, device)
+        if kind == EXPERT_AR:
+            layer, grads = req[1:]
+            return layer.replica_groups.allreduce_async(grads, layer.local_ids)
+        if kind == WAIT:
+            for w in req[1]:
+                w.wait()
+            return None
+        if kind == ALLREDUCE:
+            dist.all_reduce(req[1], group=self.group)
+            return None
+        if kind == A2A:
+            return all_to_all_rows(*req[1:], group=self.group)
+        raise ValueError(f"unknown exchange request {kind!r}")

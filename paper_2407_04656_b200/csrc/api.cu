@@ -16,3 +16,14 @@ extern "C" const char* lz_status_string(int status) {
 extern "C" int lz_version(void) { return 100; }  // 0.1.0
 
 extern "C" int lz_last_cuda_error(void) { return lzh::last_cuda_error(); }
+
+extern "C" lz_status lz_gemm_set_control_internal(lz_ctl* c);
+extern "C" lz_status lz_signal_set_control_internal(lz_ctl* c);
+
+// Every module that waits on peers or on its own pipeline keeps its own copy of the
+// control-block pointer (lz.h lz_ctl).
+extern "C" lz_status lz_set_control(lz_ctl* ctl) {
+  lz_status st = lz_gemm_set_control_internal(ctl);
+  if (st != LZ_OK) return st;
+  return lz_signal_set_control_internal(ctl);
+}

@@ -77,6 +77,50 @@ __device__ __forceinline__ T warp_sum(T v) {
   return v;
 }
 
+// ---- watchdog / abort control block (lz.h lz_ctl) ----------------------------------
+// One device-global pointer per translation unit (the .cu files are separate modules);
+// LZ_DEFINE_CTL_SETTER gives each module that waits on peers its setter, lz_set_control
+// (api.cu) calls them all.
+static __device__ lz_ctl* g_ctl = nullptr;
+
+__device__ __forceinline__ long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return (long long)t;
+}
+__device__ __forceinline__ int ld_sys_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_sys_s32(int* p, int v) {
+  asm volatile("st.relaxed.sys.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ long long ctl_timeout_ns() {
+  const lz_ctl* c = g_ctl;
+  const long long t = c ? c->timeout_ns : 0;
+  return t > 0 ? t : 10000000000ll;
+}
+// Poll step of a bounded cross-rank wait that has not succeeded yet: sleeps briefly, and
+// returns true (after recording the cause) when the wait must give up.
+__device__ __forceinline__ bool peer_wait_give_up(long long& deadline) {
+  const long long now = globaltimer_ns();
+  if (deadline == 0) deadline = now + ctl_timeout_ns();
+  lz_ctl* c = g_ctl;
+  if (c && ld_sys_s32(&c->abort)) {
+    st_sys_s32(&c->aborted, 1);
+    return true;
+  }
+  if (now > deadline) {
+    if (c) st_sys_s32(&c->timeout, 1);
+    return true;
+  }
+  // a wait that already gave up elsewhere in this step: do not stack another full timeout
+  if (c && (ld_sys_s32(&c->timeout) | ld_sys_s32(&c->aborted))) return true;
+  __nanosleep(256);
+  return false;
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -110,3 +154,11 @@ inline int num_sms() {
   return n;
 }
 }  // namespace lzh
+
+#define LZ_DEFINE_CTL_SETTER(name)                                          \
+  extern "C" lz_status name(lz_ctl* c) {                                    \
+    if (cudaMemcpyToSymbol(lz::g_ctl, &c, sizeof(c)) == cudaSuccess)        \
+      return LZ_OK;                                                         \
+    lzh::check_launch();                                                    \
+    return LZ_ERR_CUDA;                                                     \
+  }

@@ -75,7 +75,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t done = 0;
 #ifndef LZ_NO_WATCHDOG
-  // a pipeline bug must fail loudly, not hang the GPU: trap after ~10 s of waiting
+  // a pipeline bug must fail loudly, not hang the GPU: after ~10 s of waiting record it in
+  // the control block and give up (the kernel then runs to its end and the host discards
+  // the step); without a control block, trap
   const long long t0 = clock64();
 #endif
   do {
@@ -90,7 +92,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "r"(a), "r"(parity), "r"(100000)
         : "memory");
 #ifndef LZ_NO_WATCHDOG
-    if (!done && clock64() - t0 > 20000000000ll) __trap();
+    if (!done) {
+      const long long dt = clock64() - t0;
+      if (dt > (1ll << 24)) {   // slow path only (~8 ms): a healthy wait never gets here
+        lz_ctl* c = g_ctl;
+        if (c && ld_sys_s32(&c->watchdog)) return;   // another wait already gave up
+        if (dt > 20000000000ll) {
+          if (!c) __trap();
+          st_sys_s32(&c->watchdog, 1);
+          return;
+        }
+      }
+    }
 #endif
   } while (!done);
 }
@@ -482,14 +495,23 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
 // Producer side of the arrival-ordered GEMM: wait until every sender has signalled this
 // step's dispatch into our receive buffer (release stores by lz_signal_peers), then make
 // the remote rows visible to the TMA (async proxy).
+// Bounded (lz_ctl): a sender that never signals -- a rank lost mid-step -- makes the wait
+// give up after the control block's timeout (or at once when the host raises abort); the
+// GEMM then runs on whatever rows are present and the host discards the step.
 __device__ __forceinline__ void wait_arrivals(const Params& p) {
   int want;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(want) : "l"(p.epoch) : "memory");
+  long long deadline = 0;
   for (int i = 0; i < p.n_flags; ++i) {
     int v;
-    do {
+    for (;;) {
       asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(v) : "l"(p.flags + i) : "memory");
-    } while (v - want < 0);
+      if (v - want >= 0) break;
+      if (peer_wait_give_up(deadline)) {
+        i = p.n_flags;
+        break;
+      }
+    }
   }
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -1068,12 +1090,7 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 
 static int g_cta_group = 2;  // default: CTA-pair kernel
 
-// ABI compatibility: the register -> global epilogue variants were measured 1.6-2x slower
-// than smem staging + TMA stores and removed; the switch is a no-op.
-extern "C" int lz_gemm_set_direct_epilogue(int on) {
-  (void)on;
-  return 0;
-}
+LZ_DEFINE_CTL_SETTER(lz_gemm_set_control_internal)
 
 extern "C" int lz_gemm_set_cta_group(int cg) {
   if (cg == 1 || cg == 2) g_cta_group = cg;

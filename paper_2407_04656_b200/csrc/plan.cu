@@ -153,6 +153,8 @@ struct PlanArgs {
   int32_t* tab_sdelta;        // [E][N]    slot = m + sdelta
   int32_t* tab_ddelta;        // [E][N]    dest row = m + ddelta
   int d_smem;                 // T, R and D staged in shared memory (they fit)
+  int cap_rows;               // > 0: rows of every rank's receive / return buffer
+  int32_t* need_rows;         // optional: rows the largest receive / send side needs
 };
 
 // Single block.  Dynamic smem: int64 q[E] | int32 M[N][E] | int32 padoff[N][E+1]
@@ -236,6 +238,29 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   }
   __syncthreads();
 
+  // -- capacity of the exchange buffers: every rank evaluates the same plan, so every rank
+  // takes the same decision.  Rank j receives padoff[j][E] rows; sender i's rows return to
+  // its send slots (< sum_e T[e][i]).  On overflow nothing may be exchanged: the receive
+  // layout becomes empty (no GEMM tile, no pad row) and slot_kernel keeps every row local.
+  __shared__ int s_over;
+  if (tid == 0) {
+    int32_t need = 0;
+    for (int j = 0; j < N; ++j) {
+      need = max(need, s_pad[j * (E + 1) + E]);
+      int32_t sent = 0;
+      for (int e = 0; e < E; ++e) sent += Tm[e * N + j];
+      need = max(need, sent);
+    }
+    const int over = a.cap_rows > 0 && need > a.cap_rows;
+    if (over) atomicOr(a.err, LZ_ERRF_CAPACITY);
+    if (a.need_rows) *a.need_rows = need;
+    s_over = over;
+  }
+  __syncthreads();
+  if (s_over)
+    for (int x = tid; x < N * (E + 1); x += blockDim.x) s_pad[x] = 0;
+  __syncthreads();
+
   // -- slot / destination tables for this rank's assignments --------------------
   for (int x = tid; x < E * N; x += blockDim.x) {
     const int e = x / N, j = x % N;
@@ -257,19 +282,19 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
     const int e = x / N, i = x % N;
     int32_t off = s_pad[rank * (E + 1) + e];
     for (int ii = 0; ii < i; ++ii) off += Dat(ii, e, rank);
-    a.recv_src_off[e * N + i] = off;
+    a.recv_src_off[e * N + i] = s_over ? 0 : off;
     if (a.recv_stage_off) {
       int32_t st = 0;  // source-major blocks, expert-major inside a block
       for (int ii = 0; ii < i; ++ii)
         for (int ee = 0; ee < E; ++ee) st += Dat(ii, ee, rank);
       for (int ee = 0; ee < e; ++ee) st += Dat(i, ee, rank);
-      a.recv_stage_off[e * N + i] = st;
-      a.recv_cnt[e * N + i] = Dat(i, e, rank);
+      a.recv_stage_off[e * N + i] = s_over ? 0 : st;
+      a.recv_cnt[e * N + i] = s_over ? 0 : Dat(i, e, rank);
     }
   }
   for (int e = tid; e <= E; e += blockDim.x) {
     a.recv_off[e] = s_pad[rank * (E + 1) + e];
-    if (e < E) a.recv_m[e] = s_M[rank * E + e];
+    if (e < E) a.recv_m[e] = s_over ? 0 : s_M[rank * E + e];
   }
 
   // -- grid-wide exclusive scan of block histograms, one warp per expert --------
@@ -281,10 +306,24 @@ __global__ void __launch_bounds__(kSlotThreads) slot_kernel(
     const int32_t* __restrict__ blk_base, const int32_t* __restrict__ tab_pref,
     const int32_t* __restrict__ tab_sdelta, const int32_t* __restrict__ tab_ddelta,
     int32_t* __restrict__ slot, int32_t* __restrict__ gather, int32_t* __restrict__ dest_row,
-    int32_t* __restrict__ dest_rank) {
+    int32_t* __restrict__ dest_rank, int32_t* __restrict__ err, int rank, int cap_rows) {
   extern __shared__ int32_t s_cnt[];  // [kSlotWarps][E]
   const int b = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (cap_rows > 0 && (*(volatile int32_t*)err & LZ_ERRF_CAPACITY)) {
+    // the exchange buffers are too small for this plan (plan_kernel): keep every row on
+    // this rank at an in-bounds row, so the step's kernels run harmlessly and the host
+    // grows the buffers and re-runs the step
+    for (int q = threadIdx.x; q < kChunk; q += blockDim.x) {
+      const int p = b * kChunk + q;
+      if (p < P) {
+        slot[p] = p % cap_rows;
+        if (dest_row) dest_row[p] = p % cap_rows;
+        if (dest_rank) dest_rank[p] = rank;
+      }
+    }
+    return;
+  }
   for (int x = threadIdx.x; x < kSlotWarps * E; x += blockDim.x) s_cnt[x] = 0;
   __syncthreads();
   const int p_warp = b * kChunk + warp * kPerWarp;
@@ -317,13 +356,25 @@ __global__ void __launch_bounds__(kSlotThreads) slot_kernel(
     if (e >= 0) {
       const int32_t m = s_cnt[warp * E + e] + __popc(peers & lt);  // stable rank in expert e
       const int32_t* pref = tab_pref + e * (N + 1);
-      int j = 0;
-      while (pref[j + 1] <= m) ++j;  // first D[e][0] -> rank 0, next D[e][1] -> rank 1, ...
-      const int32_t s = m + tab_sdelta[e * N + j];
-      slot[p] = s;
-      gather[s] = p;
-      if (dest_row) dest_row[p] = m + tab_ddelta[e * N + j];
-      if (dest_rank) dest_rank[p] = j;
+      // The routed list must hold exactly pref[N] assignments of expert e (checked in
+      // scan_block_counts, dispatch.py:213-229); this kernel runs before the host can see
+      // that flag, so an assignment beyond its expert's schedule row is flagged here and
+      // written nowhere instead of walking past the row.
+      if (m < pref[N]) {
+        int j = 0;
+        while (j + 1 < N && pref[j + 1] <= m) ++j;  // first D[e][0] -> rank 0, next D[e][1] -> 1, ...
+        const int32_t s = m + tab_sdelta[e * N + j];
+        if (s >= 0 && s < P) {
+          slot[p] = s;
+          gather[s] = p;
+          if (dest_row) dest_row[p] = m + tab_ddelta[e * N + j];
+          if (dest_rank) dest_rank[p] = j;
+        } else {
+          atomicOr(err, LZ_ERRF_COUNTS);
+        }
+      } else {
+        atomicOr(err, LZ_ERRF_COUNTS);
+      }
     }
     __syncwarp();
     if (e >= 0 && (peers & lt) == 0) s_cnt[warp * E + e] += __popc(peers);
@@ -361,7 +412,8 @@ static size_t plan_smem(int E, int N, bool d_smem = false) {
 static bool plan_d_smem(int E, int N) { return plan_smem(E, N, true) <= 48 * 1024; }
 
 extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E, int N, int rank,
-                                      const int32_t* routed, int P, int align, int64_t* quota,
+                                      const int32_t* routed, int P, int align, int cap_rows,
+                                      int32_t* need_rows, int64_t* quota,
                                       int32_t* D, int32_t* send_sizes, int32_t* recv_sizes,
                                       int32_t* recv_counts, int32_t* slot, int32_t* gather,
                                       int32_t* dest_row, int32_t* dest_rank, int32_t* recv_m,
@@ -371,7 +423,7 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
                                       size_t ws_bytes, void* stream) {
   lz_status st = check_EN(E, N);
   if (st != LZ_OK) return st;
-  if (rank < 0 || rank >= N || P < 0 || align < 1 || !T || !R || !D || !err || !send_sizes ||
+  if (rank < 0 || rank >= N || P < 0 || align < 1 || cap_rows < 0 || !T || !R || !D || !err || !send_sizes ||
       !recv_sizes || !recv_counts || !recv_m || !recv_off || !recv_src_off)
     return LZ_ERR_ARG;
   if (P > 0 && (!routed || !slot || !gather)) return LZ_ERR_ARG;
@@ -395,7 +447,7 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
   }
   PlanArgs a{T, R, E, N, rank, align, P, B, quota, D, send_sizes, recv_sizes, recv_counts,
              recv_m, recv_off, recv_src_off, recv_stage_off, recv_cnt, err, blk_counts,
-             blk_base, pref, sdelta, ddelta, plan_d_smem(E, N) ? 1 : 0};
+             blk_base, pref, sdelta, ddelta, plan_d_smem(E, N) ? 1 : 0, cap_rows, need_rows};
   const size_t smem = plan_smem(E, N, a.d_smem != 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -403,7 +455,8 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
   if ((st = lzh::check_launch()) != LZ_OK) return st;
   if (P > 0) {
     slot_kernel<<<B, kSlotThreads, sizeof(int32_t) * kSlotWarps * E, s>>>(
-        routed, P, E, N, B, blk_base, pref, sdelta, ddelta, slot, gather, dest_row, dest_rank);
+        routed, P, E, N, B, blk_base, pref, sdelta, ddelta, slot, gather, dest_row, dest_rank, err,
+        rank, cap_rows);
     if ((st = lzh::check_launch()) != LZ_OK) return st;
   }
   return LZ_OK;
@@ -500,7 +553,8 @@ extern "C" lz_status lz_shuffle_index(const int32_t* send_counts, int E, int N,
   if ((st = lzh::check_launch()) != LZ_OK) return st;
   if (P > 0) {
     slot_kernel<<<B, kSlotThreads, sizeof(int32_t) * kSlotWarps * E, s>>>(
-        routed, P, E, N, B, blk_base, pref, sdelta, sdelta, slot, gather, nullptr, nullptr);
+        routed, P, E, N, B, blk_base, pref, sdelta, sdelta, slot, gather, nullptr, nullptr, err, 0,
+        0);
     if ((st = lzh::check_launch()) != LZ_OK) return st;
   }
   return LZ_OK;

@@ -25,9 +25,48 @@ __global__ void signal_peers_kernel(const unsigned long long* __restrict__ flag_
   }
 }
 
+// One warp: lane j publishes the new count into rank j's barrier row, then lane i waits
+// for rank i's count in ours.  Bounded by the control block (peer_wait_give_up).
+__global__ void peer_barrier_kernel(const unsigned long long* __restrict__ flag_peers, int n,
+                                    int my_rank, int* __restrict__ counter,
+                                    const int* __restrict__ own_flags) {
+  const int lane = threadIdx.x;
+  int v = 0;
+  if (lane == 0) {
+    v = *counter + 1;
+    *counter = v;   // only this kernel touches the counter, stream-ordered
+  }
+  v = __shfl_sync(0xffffffffu, v, 0);
+  __threadfence_system();   // every earlier write of this rank (incl. remote) before the flag
+  if (lane < n) {
+    int* f = reinterpret_cast<int*>(flag_peers[lane]) + my_rank;
+    asm volatile("st.release.sys.global.s32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+    long long deadline = 0;
+    for (;;) {
+      int got;
+      asm volatile("ld.acquire.sys.global.s32 %0, [%1];" : "=r"(got) : "l"(own_flags + lane)
+                   : "memory");
+      if (got - v >= 0) break;
+      if (peer_wait_give_up(deadline)) break;
+    }
+  }
+  __syncwarp();
+}
+
 }  // namespace lz
 
 using namespace lz;
+
+LZ_DEFINE_CTL_SETTER(lz_signal_set_control_internal)
+
+extern "C" lz_status lz_peer_barrier(const unsigned long long* flag_peers, int n, int my_rank,
+                                     int* counter, const int* own_flags, void* stream) {
+  if (!flag_peers || !counter || !own_flags || n < 1 || n > 32 || my_rank < 0 || my_rank >= n)
+    return LZ_ERR_ARG;
+  peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag_peers, n, my_rank, counter,
+                                                          own_flags);
+  return lzh::check_launch();
+}
 
 extern "C" lz_status lz_epoch_bump(int* epoch, void* stream) {
   if (!epoch) return LZ_ERR_ARG;

@@ -176,13 +176,25 @@ def _tr(t_matrix, replicas) -> tuple[torch.Tensor, torch.Tensor, int, int]:
     return _as_i32(t_matrix, dev), _as_i32(counts, dev), E, N
 
 
-def _raise_err(flag: int) -> None:
+class ExchangeCapacityError(RuntimeError):
+    """The plan needs more exchange-buffer rows than are allocated (LZ_ERRF_CAPACITY).
+    Every rank sees the same plan and raises together; nothing was exchanged.  Grow the
+    buffers to ``rows`` (``MoELayer.reserve``) and re-run the step."""
+
+    def __init__(self, rows: int):
+        super().__init__(f"exchange buffers too small: the plan needs {rows} rows")
+        self.rows = rows
+
+
+def _raise_err(flag: int, need: int = 0) -> None:
     if flag & _lib.LZ_ERRF_UNROUTABLE:
         raise UnroutableTokenError("an expert has routed tokens but no replicas")
     if flag & _lib.LZ_ERRF_EXPERT_ID:
         raise ValueError("token routed to unknown expert")
     if flag & _lib.LZ_ERRF_COUNTS:
         raise ValueError("routing list per-expert counts disagree with the schedule")
+    if flag & _lib.LZ_ERRF_CAPACITY:
+        raise ExchangeCapacityError(need)
 
 
 def _ws(E: int, N: int, P: int, dev) -> torch.Tensor:
@@ -211,17 +223,24 @@ class DevicePlan(NamedTuple):
     recv_src_off: torch.Tensor  # int32 [E, N]
     recv_stage_off: torch.Tensor  # int32 [E, N]
     recv_cnt: torch.Tensor     # int32 [E, N]
-    err: torch.Tensor          # int32 [1]
+    err: torch.Tensor          # int32 [2]: error bits, rows the exchange needs
 
     def check(self) -> None:
         """Synchronises; raises the reference's exception on a device error flag."""
-        _raise_err(int(self.err.item()))
+        flag, need = self.err.tolist()
+        _raise_err(flag, need)
+
+    @property
+    def need_rows(self) -> torch.Tensor:
+        return self.err[1:]
 
 
 def plan_device(T: torch.Tensor, R: torch.Tensor, rank: int, routed: torch.Tensor | None,
-                align: int = 128, stream=None) -> DevicePlan:
+                align: int = 128, stream=None, cap_rows: int = 0) -> DevicePlan:
     """Asynchronous full plan for ``rank`` on the current stream (no host sync).
-    T, R: int32 [E, N] device tensors in communicator-rank order; routed: int32 [P]."""
+    T, R: int32 [E, N] device tensors in communicator-rank order; routed: int32 [P].
+    cap_rows > 0: rows of the exchange buffers (overflow -> ExchangeCapacityError at
+    :meth:`DevicePlan.check`, identically on every rank)."""
     E, N = T.shape
     dev = T.device
     P = 0 if routed is None else routed.numel()
@@ -236,10 +255,11 @@ def plan_device(T: torch.Tensor, R: torch.Tensor, rank: int, routed: torch.Tenso
     recv_m = torch.empty(E, **i32)
     recv_off = torch.empty(E + 1, **i32)
     recv_src_off, recv_stage_off, recv_cnt = (torch.empty((E, N), **i32) for _ in range(3))
-    err = torch.zeros(1, **i32)
+    err = torch.zeros(2, **i32)
     ws = _ws(E, N, P, dev)
     _lib.call("lz_plan_dispatch", _lib.ptr(T), _lib.ptr(R), E, N, rank,
-              _lib.ptr(routed) if P else None, P, align, _lib.ptr(quota), _lib.ptr(D),
+              _lib.ptr(routed) if P else None, P, align, int(cap_rows), err[1:].data_ptr(),
+              _lib.ptr(quota), _lib.ptr(D),
               _lib.ptr(send_sizes), _lib.ptr(recv_sizes), _lib.ptr(recv_counts),
               _lib.ptr(slot) if P else None, _lib.ptr(gather) if P else None,
               _lib.ptr(dest_row) if P else None, _lib.ptr(dest_rank) if P else None,
@@ -349,7 +369,7 @@ def simulate_all_to_all(schedules: Sequence[DispatchSchedule]) -> list[list[list
 
 
 __all__ = [
-    "DevicePlan", "DispatchConsistencyError", "DispatchSchedule", "ReplicaMatrix",
+    "DevicePlan", "DispatchConsistencyError", "ExchangeCapacityError", "DispatchSchedule", "ReplicaMatrix",
     "UnroutableTokenError", "build_shuffle_index", "compute_dispatch_schedule",
     "full_dispatch_matrices", "gather_load_matrix", "invert_permutation", "plan_device",
     "simulate_all_to_all",

@@ -216,6 +216,12 @@ def epoch_bump(epoch) -> None:
     _lib.call("lz_epoch_bump", ptr(epoch), _s())
 
 
+def peer_barrier(flag_peers, n: int, my_rank: int, counter, own_flags, stream=None) -> None:
+    """Device-side cross-rank barrier (bounded by the watchdog control block)."""
+    _lib.call("lz_peer_barrier", ptr(flag_peers), int(n), int(my_rank), ptr(counter),
+              ptr(own_flags), _lib.stream_ptr(stream))
+
+
 def signal_peers(flag_peers, n: int, my_rank: int, epoch) -> None:
     """Publish this step's epoch in every rank's arrival-flag slot for this sender."""
     _lib.call("lz_signal_peers", ptr(flag_peers), int(n), int(my_rank), ptr(epoch), _s())

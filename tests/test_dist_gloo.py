@@ -128,3 +128,69 @@ def test_elastic_replan_and_transfers():
                  if R[e][r] > 0 and e not in held[v]}
         assert newly == {(e, dst) for e, _, dst in transfers} | {(e, v) for e, v in orphans}
         holdings = {v: {e for e in range(E) if R[e][r] > 0} for r, v in enumerate(sorted(live))}
+
+
+def _migrate_worker(rank, n, port, q):
+    """Two CPU ranks with MoELayer objects (no kernels run: construction and set_plan are
+    host/tensor work): rank 1 newly hosts expert 0, whose weights and Adam moments must
+    arrive from rank 0 over gloo send/recv, and the optimizer must follow the new
+    Parameters (elastic.exchange_expert_state + remap_optimizer, PAPER.md:417)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        from paper_2407_04656_b200.elastic import exchange_expert_state, remap_optimizer
+        from paper_2407_04656_b200.layer import MoELayer
+        E, d, dff = 4, 256, 256
+        R0 = [[1, 0], [1, 1], [0, 1], [0, 1]]       # expert 0 only on rank 0
+        layer = MoELayer(d, dff, E, 2, replicas=R0, group=dist.group.WORLD, device="cpu",
+                         seed=7, activation="swiglu")
+        opt = torch.optim.Adam([layer.w1, layer.w2], lr=1e-2)
+        layer.w1.grad = torch.full_like(layer.w1, 0.5 + rank)
+        layer.w2.grad = torch.full_like(layer.w2, -0.25)
+        opt.step()
+        before = {e: [t.clone() for t in ts] for e, ts in
+                  __import__("paper_2407_04656_b200.elastic", fromlist=["x"])
+                  .expert_slices(layer, opt).items()}
+        R1 = [[1, 1], [1, 1], [0, 1], [0, 1]]       # rank 1 now also hosts expert 0
+        slices = exchange_expert_state([layer], [((0, 0), 0, 1)], rank, {0: 0, 1: 1},
+                                       dist.group.WORLD, [opt])[0]
+        info = layer.set_plan(R1, weights={e: (v[0], v[1]) for e, v in slices.items()})
+        remap_optimizer(opt, layer, info, slices)
+        assert opt.param_groups[0]["params"][0] is layer.w1
+        got = {e: [layer.w1.data[p], layer.w2.data[p],
+                   opt.state[layer.w1]["exp_avg"][p], opt.state[layer.w1]["exp_avg_sq"][p],
+                   opt.state[layer.w2]["exp_avg"][p], opt.state[layer.w2]["exp_avg_sq"][p]]
+               for p, e in enumerate(layer.local_ids)}
+        # send rank 0's expert-0 state to the test for comparison with rank 1's copy
+        q.put((rank, {e: [t.tolist() for t in v] for e, v in got.items() if e == 0},
+               {e: [t.tolist() for t in v] for e, v in before.items() if e == 0},
+               layer.local_ids, int(opt.state[layer.w1]["step"])))
+        opt.step()   # the optimizer keeps stepping the live parameters
+    except Exception as exc:  # pragma: no cover - surfaced by the parent
+        q.put((rank, repr(exc), None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_expert_state_migration_moves_optimizer_state():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, got, before, ids, step = q.get(timeout=300)
+        assert not isinstance(got, str), got
+        res[r] = (got, before, ids, step)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1][2] == [0, 1, 2, 3] and res[0][2] == [0, 1]
+    src = res[0][1][0]     # rank 0's expert 0 before the move: w1, w2, 4 moments
+    dst = res[1][0][0]     # rank 1's expert 0 after the move
+    assert len(src) == 6 and src == dst
+    assert res[1][3] == 1
