@@ -201,3 +201,31 @@ def recv_layout(D_all, rank: int, align: int = 1):
     for e in range(E):
         src_off[e] = pad_off[e] + np.concatenate([[0], np.cumsum(D[:, e, rank])[:-1]])
     return m, pad_off, src_off
+
+
+def adaptive_layer_cost(R, layer_tokens: Sequence[int], n_ranks: int) -> tuple[int, int]:
+    """(max per-node compute tokens, cross-node tokens) of one layer under the flexible
+    dispatch, tokens split uniformly over the ranks.  simulator.py:198-219 (R is
+    ReplicaMatrix.from_plan(plan).counts, dispatch.py:40-47)."""
+    T = [split_proportionally(int(t), [1] * n_ranks) for t in layer_tokens]
+    D = full_dispatch_matrices(T, R)
+    node = [0] * n_ranks
+    cross = 0
+    for i in range(n_ranks):
+        for row in D[i]:
+            for j in range(n_ranks):
+                node[j] += row[j]
+                if j != i:
+                    cross += row[j]
+    return max(node), cross
+
+
+def step_time_adaptive(Rs: dict, layer_loads: dict, n_ranks: int, alpha: float, beta: float,
+                       overhead: float) -> float:
+    """step_time_model(strategy="adaptive") (simulator.py:248-266): overhead +
+    sum over layers (sorted) of alpha * max_node + beta * cross."""
+    total = overhead
+    for layer, tokens in sorted(layer_loads.items()):
+        max_node, cross = adaptive_layer_cost(Rs[layer], tokens, n_ranks)
+        total += alpha * max_node + beta * cross
+    return total

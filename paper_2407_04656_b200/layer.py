@@ -245,6 +245,13 @@ class MoELayer(torch.nn.Module):
         return _MoEFunction.apply(x, self.wg, self.bg, self.w1, self.w2, self)
 
     # ------------------------------------------------------------- stats
+    def layer_cost(self) -> tuple[int, int]:
+        """(max node tokens, cross-node tokens) of the last plan on its real routing --
+        the two terms of the reference's time model (simulator.py:198-219, cost.py)."""
+        from .cost import plan_cost
+        mx, cross = plan_cost(self.last_plan.D)
+        return int(mx), int(cross)
+
     def imbalance(self) -> float:
         """max_j recv_j / mean_j recv_j of the last plan."""
         p = self.last_plan

@@ -201,10 +201,10 @@ def test_loopback_capacity_overflow_then_reserve():
     ExchangeCapacityError (nothing exchanged, no out-of-bounds write), reserve() grows the
     buffers, and the re-run step matches the oracle."""
     from paper_2407_04656_b200.dispatch import ExchangeCapacityError
-    N, E, k, d, dff, Tn = 4, 16, 2, 512, 1024, 512
+    N, E, k, d, dff, Tn = 4, 8, 2, 256, 512, 4096
     world, layers, R = _world(N, E, k, d, dff, "gelu", 2.5, slot_factor=1)
     for L in layers:
-        L.capacity_slack = 0.3
+        L.capacity_slack = 0.3     # 0.3 x 8192 rows + 8 x 255 padding < the hot rank's rows
     xs, douts = _inputs(N, Tn, d)
     world.step(layers, xs)
     torch.cuda.synchronize()
