@@ -30,7 +30,7 @@ CONFIGS = {
     # name: E, k, d, d_ff, tokens per GPU, zipf s, slot factor (c = ceil(f*E/N)), bwd.
     # slot_factor 6 (cfg2/cfg5): with Zipf(1.2) top-2 loads the reference's MRO plans reach
     # max/mean receive 1.07 at N = 4 (factor 5: 1.15, 3: 1.49)
-    "cfg1": dict(E=8, k=2, d=512, dff=2048, tokens=1024, s=1.2, slot_factor=2, bwd=False,
+    "cfg1": dict(E=8, k=2, d=512, dff=2048, tokens=1024, s=1.2, slot_factor=2, bwd=False, virtual=4,
                  name="CPU-ref MoE layer (E8 top-2 d512 d_ff2048, 1024 tok/rank, fwd)"),
     "cfg2": dict(E=16, k=2, d=1024, dff=4096, tokens=65536, s=1.2, slot_factor=6, bwd=True,
                  name="GPT-MoE layer (E16 top-2 d1024 d_ff4096, 64K tok/GPU, fwd+bwd)"),
@@ -135,19 +135,39 @@ def cpu_model() -> str:
 
 
 def cpu_reference(cfg, n_ranks, tokens_per_rank, reps, threads, seed=0):
-    """Reference path on the host cores (oracle port).  Returns (tokens/s, seconds, tokens)."""
+    """Reference path on the host cores (oracle/cpu_path.py: flexep unchanged from
+    baseline/_ref for the integer stages when present, else the pinned port; torch-CPU
+    fp32 float stages).  Returns (tokens/s, seconds, tokens, kind)."""
     from oracle import cpu_path
-    from paper_2407_04656_b200.layer import zipf_router_bias
-    from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix
     E = cfg["E"]
-    bias = zipf_router_bias(E, cfg["s"], seed)
+    bias = _zipf_bias(E, cfg["s"], seed)
     p = torch.softmax(bias, 0).tolist()
     loads = [max(1, int(v * tokens_per_rank * n_ranks * cfg["k"])) for v in p]
-    c = math.ceil(cfg["slot_factor"] * E / n_ranks)
-    R = replica_matrix(plan_for_loads(loads, n_ranks, c, 2))
-    return cpu_path.run(tokens_per_rank, n_ranks, E, cfg["d"], cfg["dff"], cfg["k"], R, reps=reps,
-                        seed=seed, bias=bias, backward=cfg["bwd"], threads=threads,
-                        activation=cfg.get("act", "gelu"))
+    return cpu_path.run(tokens_per_rank, n_ranks, E, cfg["d"], cfg["dff"], cfg["k"], loads,
+                        cpu_path.slots_for(cfg, n_ranks), 2, reps=reps, seed=seed, bias=bias,
+                        backward=cfg["bwd"], threads=threads, activation=cfg.get("act", "gelu"))
+
+
+def _zipf_bias(E, s, seed=0):
+    """log p_e, p_e ~ (1 + pi(e))^-s (the synthetic routing of SURVEY.md 8d; the same
+    formula as layer.zipf_router_bias, restated so the reference arm imports nothing of
+    the product)."""
+    g = torch.Generator().manual_seed(seed)
+    perm = torch.randperm(E, generator=g).float()
+    p = (1.0 + perm) ** (-s)
+    return torch.log(p / p.sum())
+
+
+def reference_sample(cfg, world):
+    """(simulated ranks, tokens per rank) of one reference-arm step: the GPU arm's per-GPU
+    step (cfg2: 65,536 tokens fwd+bwd) -- at N = 1 exactly the measured configuration;
+    at N > 1 the same tokens spread over N simulated ranks (the N-rank plan).  cfg1: the
+    full config (4 simulated ranks x 1024 tokens).  cfg3 (a CPU step > 30 s): a sample."""
+    if "cpu_tokens" in cfg:
+        return 1, cfg["cpu_tokens"]
+    if cfg.get("virtual"):
+        return cfg["virtual"], cfg["tokens"]
+    return world, cfg["tokens"] // world
 
 
 def run_reference(args, cfg):
@@ -156,28 +176,35 @@ def run_reference(args, cfg):
         return 0
     threads = len(os.sched_getaffinity(0))
     torch.set_num_threads(threads)
-    sample = cfg.get("cpu_tokens", 2048) if cfg["bwd"] else cfg["tokens"]
-    n_virtual = 1 if args.config != "cfg1" else 4
-    per_rank = sample // n_virtual if args.config != "cfg1" else cfg["tokens"]
+    n_sim, per_rank = reference_sample(cfg, world)
+    # warm-up steps on a small sample (allocator / thread-pool warm-up; untimed)
     for _ in range(args.warmup):
-        cpu_reference(cfg, n_virtual, per_rank, 1, threads)
+        cpu_reference(cfg, n_sim, min(per_rank, 1024), 1, threads)
     times = []
     tok = 0
+    kind = "port"
     for _ in range(args.steps):
-        _, dt, t = cpu_reference(cfg, n_virtual, per_rank, 1, threads)
+        _, dt, t, kind = cpu_reference(cfg, n_sim, per_rank, 1, threads)
         times.append(dt)
         tok += t
     total = sum(times)
     value = tok / total
+    same = "cpu_tokens" not in cfg and (world == 1 or bool(cfg.get("virtual")))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["name"], "sample_tokens_per_step": tok // args.steps},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+        "config": {"workload": cfg["name"], "simulated_ranks": n_sim,
+                   "tokens_per_step": tok // args.steps, "same_as_gpu_arm": bool(same)},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": kind,
                          "cpu_model": cpu_model(),
-                         "sample": f"{tok // args.steps} tokens per step x {args.steps} steps"},
+                         "integer_stages": "flexep 0.1.0 unchanged (baseline/_ref)"
+                         if kind == "reference" else "oracle port (pinned to reference goldens)",
+                         "float_stages": "torch-CPU fp32 restatement (the reference has none)",
+                         "sample": f"{tok // args.steps} tokens per step ({n_sim} simulated "
+                                   f"rank(s)) x {args.steps} steps; warm-up on 1024-token "
+                                   f"samples"},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -210,8 +237,13 @@ def run_gpu(args, cfg):
     g.manual_seed(1234 + rank)
     x = torch.randn(Tn, d, generator=g, device=dev).bfloat16()
     dout = (torch.randn(Tn, d, generator=g, device=dev) * 1e-2).bfloat16()
-    # load-based replicas from this batch's routing (the paper rebalances from history)
-    _, _, _, hist = ops.router_gate(x, layer.wg.detach(), layer.bg.detach(), k)
+    # load-based replicas from the routing of a SEPARATE batch of the same distribution
+    # (the paper re-plans from a history window, not from the batch it then runs)
+    gp = torch.Generator(device=dev)
+    gp.manual_seed(777 + rank)
+    x_plan = torch.randn(Tn, d, generator=gp, device=dev).bfloat16()
+    _, _, _, hist = ops.router_gate(x_plan, layer.wg.detach(), layer.bg.detach(), k)
+    del x_plan
     hist = hist.long()
     if world > 1:
         dist.all_reduce(hist)
@@ -233,6 +265,7 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     layer.check()
     imbalance = layer.imbalance()
+    max_node_tokens, cross_node_tokens = layer.layer_cost()   # simulator.py:198-219 terms
     rows_local = int(layer.last_plan.recv_m.sum())  # assignments this rank's experts process
     x_h = x.cpu().pin_memory()
     d_h = dout.cpu().pin_memory()
@@ -241,13 +274,13 @@ def run_gpu(args, cfg):
     # step is captured once and replayed; value/ms_per_step/e2e come from it, the eager
     # numbers measured afterwards are reported alongside (graph first: sustained
     # power/thermal settling only ever penalises the later measurement).
-    graph, graph_err = None, ""
+    graph, graph_err, in_graph = None, "", None
     if args.no_graph:
         graph_err = "graphs disabled"
     else:
         from paper_2407_04656_b200.graphs import GraphedStep
         try:
-            graph = GraphedStep(layer, Tn, nbuf=2, backward=cfg["bwd"])
+            graph = GraphedStep(layer, Tn, nbuf=2, backward=cfg["bwd"], timed_slot=1)
         except Exception as exc:  # report, keep eager numbers
             import traceback
             traceback.print_exc()
@@ -311,6 +344,21 @@ def run_gpu(args, cfg):
             t = torch.tensor([ms_graph, ms_graph_e2e], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms_graph, ms_graph_e2e = (float(v) for v in t.tolist())
+        # the GEMMs timed from inside the graph: slot 1 carries event-record nodes around
+        # the step and every grouped-GEMM launch; each replay is read back, so the GEMM
+        # time and the step time come from the same replays
+        for b in range(2):
+            graph.x[b].copy_(x)
+            graph.dout[b].copy_(dout)
+        rt = graph.replay_times(args.steps)
+        in_graph = {"step_ms": float(np.median(rt["step_ms"])),
+                    "gemm_ms": float(np.median(rt["gemm_ms"])),
+                    "gemm_launch_ms": [float(np.median(c)) for c in zip(*rt["gemm_launch_ms"])]}
+        if world > 1:
+            t = torch.tensor([in_graph["step_ms"], in_graph["gemm_ms"]], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            in_graph["step_ms_max_over_ranks"], in_graph["gemm_ms_max_over_ranks"] = \
+                (float(v) for v in t.tolist())
         # autograd nodes created under capture stay bound to the capture stream and would
         # force a device sync on every later eager backward: continue on a fresh layer
         # object with identical weights and plan
@@ -332,7 +380,7 @@ def run_gpu(args, cfg):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ops.GEMM_EVENTS = []
+    ops.GEMM_EVENTS = [] if in_graph is None else None
     l0 = _lib.launch_count
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -342,9 +390,11 @@ def run_gpu(args, cfg):
     torch.cuda.synchronize()
     launches = _lib.launch_count - l0
     ms = e0.elapsed_time(e1)
-    gemm_ms = sum(a.elapsed_time(b) for a, b in ops.GEMM_EVENTS)
-    n_gemm = len(ops.GEMM_EVENTS)
-    ops.GEMM_EVENTS = None
+    if in_graph is None:   # eager only: GEMM events of the timed eager steps
+        gemm_ms = sum(a.elapsed_time(b) for a, b in ops.GEMM_EVENTS)
+        ops.GEMM_EVENTS = None
+    else:
+        gemm_ms = in_graph["gemm_ms"] * args.steps
     if world > 1:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -443,9 +493,9 @@ def run_gpu(args, cfg):
             "dispatch_bwd": Pa * d * 2 + Tn * d * 2 + 2 * Tn * E * 4,
             "router_wgrad": Tn * d * 2 + Tn * E * 4,
         }
-        if getattr(layer, "tail_overlap", False) and world == 1 and cfg["bwd"]:
-            # these two run on a side stream under the weight-gradient GEMMs: their time
-            # is inside `ffn_bwd` (isolated numbers: hbm_kernels)
+        if getattr(layer, "tail_overlap", False) and cfg["bwd"]:
+            # these two run on a side stream under the weight-gradient GEMMs (their stage
+            # marks time them there, slowed by the GEMMs; isolated numbers: hbm_kernels)
             stage_bytes.pop("dispatch_bwd")
             stage_bytes.pop("router_wgrad")
         hbm_stages = {}
@@ -492,6 +542,12 @@ def run_gpu(args, cfg):
                        "slots_per_gpu": c, "fault_threshold": 2, "zipf_s": cfg["s"],
                        "replicas": list(plan_replicas(plan, E)),
                        "imbalance_max_over_mean_recv": round(imbalance, 4),
+                       "reference_cost_terms": {"max_node_tokens": max_node_tokens,
+                                                "cross_node_tokens": cross_node_tokens,
+                                                "model": "flexep simulator.py:198-219 "
+                                                         "(adaptive_layer_cost) on this "
+                                                         "step's device plan"},
+                       "replica_plan_source": "routing histogram of a separate batch",
                        "l2": "inputs larger than L2 (x alone 134 MB; step working set > 4 GB)",
                        "parallelism": f"flexible-EP{world} (DP tokens, replicated experts)"},
             "roofline": {"kernel": "lz grouped_gemm (tcgen05 fwd+dgrad+wgrad)", "bound": "tensor",
@@ -502,7 +558,14 @@ def run_gpu(args, cfg):
                          "peak_kind": f"{src} sustained bf16",
                          "flops_per_launch": flops_per_launch,
                          "gemm_ms_per_step": gemm_ms / args.steps,
-                         "gemm_share_of_step": gemm_ms / ms if ms else None,
+                         "gemm_share_of_step": (in_graph["gemm_ms"] / in_graph["step_ms"])
+                         if in_graph else gemm_ms / ms,
+                         "timing": "graph event-record nodes around every GEMM launch and "
+                                   "the whole step, read after each of K replays of the "
+                                   "captured step (medians; same replays for both)"
+                         if in_graph else "CUDA events around the GEMM launches of the "
+                                          "timed eager steps",
+                         "in_graph": in_graph,
                          "gemms_per_step": gemms_per_step},
             "mode": "cuda-graph replay of the whole fwd+bwd step" if graph is not None
                     else "eager (" + graph_err + ")",
@@ -531,15 +594,15 @@ def run_gpu(args, cfg):
         }
         if world == 1 and not args.no_cpu_baseline:
             threads = len(os.sched_getaffinity(0))
-            ctok = cfg.get("cpu_tokens", 4096 if cfg["bwd"] else Tn)
-            reps = cfg.get("cpu_reps", args.cpu_reps)
-            tps, dt, tok = cpu_reference(cfg, 1, ctok, reps, threads)
+            n_sim, ctok = reference_sample(cfg, 1)
+            cpu_reference(cfg, n_sim, min(ctok, 1024), 1, threads)   # warm-up
+            tps, dt, tok, kind = cpu_reference(cfg, n_sim, ctok, 1, threads)
             line["cpu_baseline"] = {"value": tps, "unit": "tokens/s", "cores": threads,
-                                    "cpu_model": cpu_model(),
-                                    "kind": "port",
-                                    "sample": f"{tok} tokens ({reps} x {ctok}) of the "
-                                              f"same layer {'fwd+bwd' if cfg['bwd'] else 'fwd'} "
-                                              f"on 1 rank, {dt:.1f} s"}
+                                    "cpu_model": cpu_model(), "kind": kind,
+                                    "sample": f"{tok} tokens: one full "
+                                              f"{'fwd+bwd' if cfg['bwd'] else 'fwd'} step of the "
+                                              f"same layer on 1 rank (the --impl reference "
+                                              f"step), {dt:.1f} s"}
         emit(line)
     if world > 1:
         dist.destroy_process_group()
@@ -689,7 +752,7 @@ def run_virtual(args, cfg):
         cpu_reference(cfg, nv, Tn, 1, threads)
         vals = [cpu_reference(cfg, nv, Tn, 1, threads) for _ in range(max(1, args.cpu_reps // 4))]
         cpu = {"value": sum(v[2] for v in vals) / sum(v[1] for v in vals), "unit": "tokens/s",
-               "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+               "cores": threads, "kind": vals[0][3], "cpu_model": cpu_model(),
                "sample": f"full config 1 ({tokens} tokens, 4 simulated ranks) x {len(vals)}"}
     flops = 2 * tokens * k * d * dff * 2
     line = {"metric": METRIC.replace("fwd+bwd", "fwd"), "value": tokens / (ms * 1e-3),

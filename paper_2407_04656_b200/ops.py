@@ -134,16 +134,19 @@ def router_wgrad(dlogits, x, with_bias: bool = True):
 
 
 # Optional timing hook: when set to a list, every grouped-GEMM launch appends a
-# (start, end) pair of CUDA events recorded on the launching stream (bench.py).
+# (start, end) pair of CUDA events recorded on the launching stream (bench.py).  Under
+# CUDA-graph capture set GEMM_EVENTS_EXTERNAL: the events become event-record nodes of
+# the graph and time the GEMMs of every replay.
 GEMM_EVENTS: list | None = None
+GEMM_EVENTS_EXTERNAL = False
 
 
 def _gemm(*args, fn: str = "lz_grouped_gemm"):
     if GEMM_EVENTS is None:
         _lib.call(fn, *args)
         return
-    a = torch.cuda.Event(enable_timing=True)
-    b = torch.cuda.Event(enable_timing=True)
+    a = torch.cuda.Event(enable_timing=True, external=GEMM_EVENTS_EXTERNAL)
+    b = torch.cuda.Event(enable_timing=True, external=GEMM_EVENTS_EXTERNAL)
     a.record()
     _lib.call(fn, *args)
     b.record()
