@@ -74,11 +74,12 @@ def _rows(Tn, k, n_rows, gen):
     return torch.randperm(n_rows, generator=gen)[:Tn * k].int()
 
 
+@pytest.mark.parametrize("d", [1024, 2048])   # cfg2 / cfg4 model widths
 @pytest.mark.parametrize("m,off", [([2500, 0, 3500], [0, 2560, 2560, 6144]),      # 128-aligned
                                    ([2049, 0, 3951], [0, 2304, 2304, 6400])])     # pads up to 255
-def test_pack_exact_and_pad_zero(m, off):
+def test_pack_exact_and_pad_zero(m, off, d):
     gen = torch.Generator().manual_seed(5)
-    Tn, d, k = 3000, 1024, 2
+    Tn, k = 3000, 2
     x = torch.randn(Tn, d, generator=gen).bfloat16()
     mt = torch.tensor(m, dtype=torch.int32)
     ot = torch.tensor(off, dtype=torch.int32)
@@ -92,9 +93,10 @@ def test_pack_exact_and_pad_zero(m, off):
     assert torch.equal(out.cpu(), ref)
 
 
-def test_combine_and_backward():
+@pytest.mark.parametrize("d,k", [(1024, 2), (2048, 1), (2048, 2)])
+def test_combine_and_backward(d, k):
     gen = torch.Generator().manual_seed(6)
-    Tn, d, k, E = 2048, 1024, 2, 16
+    Tn, E = 2048, 16
     n_rows = Tn * k + 512
     y = torch.randn(n_rows, d, generator=gen).bfloat16()
     row = _rows(Tn, k, n_rows, gen)

@@ -100,7 +100,10 @@ def _zipf_routing(rng, E, P, s):
 
 @pytest.mark.parametrize("E,N,P,s,c", [(16, 8, 131072, 1.2, 6), (8, 4, 2048, 1.2, 4),
                                        (64, 8, 131072, 1.5, 32), (16, 1, 131072, 1.2, 48),
-                                       (3, 5, 777, 0.0, 2)])
+                                       (3, 5, 777, 0.0, 2),
+                                       # cfg4's largest single-GPU size: E64 top-1, 1M tokens
+                                       (64, 1, 1048576, 1.5, 256),
+                                       (64, 8, 1048576, 1.5, 32)])
 def test_plan_device_scale(E, N, P, s, c):
     """B200-scale instances: every rank's D, sizes, slot/gather (= reference shuffle
     index) and receive layout agree exactly with the oracle."""

@@ -1,0 +1,162 @@
+"""Vendor bar for the grouped expert GEMMs: the lz tcgen05
+grouped GEMM against torch._grouped_mm (CUTLASS), flashinfer's cuDNN grouped_mm_bf16 and
+(forward of a whole MoE layer) flashinfer's fused MoE kernels, in ONE process on the same
+B200, on the BASELINE cfg2 / cfg3 shapes with a Zipf(1.2) routing histogram.
+
+    python tools/vendor_bar.py [--json out.json]
+
+Every kernel is timed with CUDA events over 20 back-to-back launches after warm-up;
+TFLOP/s are algorithmic (2 M N K per group, unpadded rows).  The vendor kernels get
+the unpadded group sizes; lz gets its 256-row padded segments (the padding rows are
+computed but not credited).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2407_04656_b200 import _lib, ops  # noqa: E402
+from paper_2407_04656_b200.layer import zipf_router_bias  # noqa: E402
+
+
+def timeit(fn, reps=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def group_sizes(E, k, T, s, seed=0):
+    g = torch.Generator().manual_seed(seed)
+    bias = zipf_router_bias(E, s, seed=0)
+    logits = bias + (-torch.log(-torch.log(torch.rand(T, E, generator=g))))
+    idx = logits.topk(k, dim=1).indices
+    return torch.bincount(idx.view(-1), minlength=E).tolist()
+
+
+def run_shape(name, E, k, T, d, dff, s, out):
+    dev = torch.device("cuda")
+    m = group_sizes(E, k, T, s)
+    P = sum(m)
+    align = ops.row_align()
+    mp = [(v + align - 1) // align * align for v in m]
+    rows_p = sum(mp)
+    off_p = torch.tensor([0] + list(torch.tensor(mp).cumsum(0)), dtype=torch.int32, device=dev)
+    offs_u = torch.tensor(list(torch.tensor(m).cumsum(0)), dtype=torch.int32, device=dev)
+    indptr_u = torch.tensor([0] + list(torch.tensor(m).cumsum(0)), dtype=torch.int32, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1)
+    X = torch.randn(rows_p, d, generator=g, device=dev).bfloat16()
+    W1 = (torch.randn(E, dff, d, generator=g, device=dev) * 0.02).bfloat16()   # [E, N, K]
+    W2 = (torch.randn(E, d, dff, generator=g, device=dev) * 0.02).bfloat16()
+    A = torch.randn(rows_p, dff, generator=g, device=dev).bfloat16()
+    dY = torch.randn(rows_p, d, generator=g, device=dev).bfloat16()
+    Xu, Au, dYu = X[:P].contiguous(), A[:P].contiguous(), dY[:P].contiguous()
+    res = {"shape": name, "E": E, "k": k, "tokens": T, "d": d, "d_ff": dff, "rows": P,
+           "group_rows": m}
+    f1 = 2.0 * P * d * dff
+
+    def rec(kind, impl, ms, flops):
+        res.setdefault(kind, {})[impl] = {"ms": round(ms, 4), "TFLOPs": round(flops / ms / 1e9, 1)}
+
+    # ---- forward GEMM1: [P, d] x W1^T -> [P, d_ff]
+    C1 = torch.empty(rows_p, dff, dtype=torch.bfloat16, device=dev)
+    rec("fwd1", "lz", timeit(lambda: ops.grouped_gemm_rows(X, W1, off_p, C1)), f1)
+    W1t = W1.transpose(1, 2)     # [E, K, N] view, K-major per expert
+    try:
+        rec("fwd1", "torch._grouped_mm", timeit(lambda: torch._grouped_mm(Xu, W1t, offs=offs_u)), f1)
+    except Exception as exc:
+        res.setdefault("errors", {})["torch._grouped_mm fwd1"] = repr(exc)[:200]
+    try:
+        from flashinfer.grouped_mm import grouped_mm_bf16
+        rec("fwd1", "flashinfer.grouped_mm_bf16(cudnn)",
+            timeit(lambda: grouped_mm_bf16(Xu, W1, indptr_u)), f1)
+    except Exception as exc:
+        res.setdefault("errors", {})["flashinfer fwd1"] = repr(exc)[:200]
+    # ---- forward GEMM2: [P, d_ff] x W2^T -> [P, d]
+    C2 = torch.empty(rows_p, d, dtype=torch.bfloat16, device=dev)
+    rec("fwd2", "lz", timeit(lambda: ops.grouped_gemm_rows(A, W2, off_p, C2)), f1)
+    W2t = W2.transpose(1, 2)
+    try:
+        rec("fwd2", "torch._grouped_mm", timeit(lambda: torch._grouped_mm(Au, W2t, offs=offs_u)), f1)
+    except Exception as exc:
+        res.setdefault("errors", {})["torch._grouped_mm fwd2"] = repr(exc)[:200]
+    # ---- weight gradient: dW2_e = dY_e^T A_e  ([d, d_ff] per expert, K = rows_e)
+    dW2 = torch.empty(E, d, dff, dtype=torch.bfloat16, device=dev)
+    rec("wgrad2", "lz", timeit(lambda: ops.grouped_gemm_wgrad(dY, A, off_p, dW2)), f1)
+    dYt = dYu.t().contiguous()   # [d, P]: torch's 2d x 2d form wants K (= P) contiguous in A
+    try:
+        rec("wgrad2", "torch._grouped_mm",
+            timeit(lambda: torch._grouped_mm(dYt, Au, offs=offs_u)), f1)
+    except Exception as exc:
+        res.setdefault("errors", {})["torch._grouped_mm wgrad2"] = repr(exc)[:200]
+    out.append(res)
+    print(json.dumps(res), flush=True)
+
+
+def run_fused_moe(out):
+    """Whole-layer forward (routing given) of the Mixtral shape: lz (pack + 2 grouped GEMMs
+    with the SwiGLU epilogue + combine) vs flashinfer's fused MoE kernels."""
+    from paper_2407_04656_b200.layer import MoELayer
+    dev = torch.device("cuda")
+    E, k, T, d, dff = 8, 2, 16384, 4096, 14336
+    res = {"shape": "cfg3 forward (routing given)", "E": E, "k": k, "tokens": T, "d": d,
+           "d_ff": dff}
+    layer = MoELayer(d, dff, E, k, seed=0, activation="swiglu", device=dev,
+                     router_bias=zipf_router_bias(E, 1.2), router_std=1.28 / math.sqrt(d))
+    x = torch.randn(T, d, device=dev).bfloat16()
+    flops = 2.0 * T * k * d * dff * 3
+    with torch.no_grad():
+        res["lz_layer_fwd"] = {"ms": round(timeit(lambda: layer(x)), 4)}
+    res["lz_layer_fwd"]["TFLOPs"] = round(flops / res["lz_layer_fwd"]["ms"] / 1e9, 1)
+    idx, w, _, _ = ops.router_gate(x, layer.wg.detach(), layer.bg.detach(), k)
+    try:
+        from flashinfer.fused_moe import cutlass_fused_moe
+        # flashinfer's layout: fc1 [E, 2 d_ff, d] (W3 | W1 for Swiglu), fc2 [E, d, d_ff]
+        fc1 = (torch.randn(E, 2 * dff, d, device=dev) * 0.02).bfloat16()
+        fc2 = (torch.randn(E, d, dff, device=dev) * 0.02).bfloat16()
+        outb = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        fn = lambda: cutlass_fused_moe(x, idx, w, fc1, fc2, torch.bfloat16, [],  # noqa: E731
+                                       output=outb)
+        ms = timeit(fn)
+        res["flashinfer.cutlass_fused_moe"] = {"ms": round(ms, 4),
+                                               "TFLOPs": round(flops / ms / 1e9, 1)}
+    except Exception as exc:
+        res.setdefault("errors", {})["cutlass_fused_moe"] = repr(exc)[:300]
+    out.append(res)
+    print(json.dumps(res), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--json", default=None)
+    ap.add_argument("--no-fused", action="store_true")
+    args = ap.parse_args()
+    _lib.load()
+    out = []
+    run_shape("cfg2", 16, 2, 65536, 1024, 4096, 1.2, out)
+    run_shape("cfg3", 8, 2, 16384, 4096, 14336, 1.2, out)
+    if not args.no_fused:
+        run_fused_moe(out)
+    if args.json:
+        with open(args.json, "w") as f:
+            json.dump({"gpu": torch.cuda.get_device_name(), "results": out}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
