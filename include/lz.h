@@ -321,6 +321,14 @@ lz_status lz_signal_peers(const unsigned long long* flag_peers, int n, int my_ra
  * control block (lz_set_control): on timeout / abort it records the cause and returns. */
 lz_status lz_peer_barrier(const unsigned long long* flag_peers, int n, int my_rank, int* counter,
                           const int* own_flags, void* stream);
+/* The same barrier for n_local ranks that share ONE GPU (single-GPU loopback of the
+ * multi-rank path), as ONE launch with one warp per co-hosted rank -- ranks that wait on
+ * each other must never be separate launches on one GPU (nothing makes them co-resident).
+ * Warp w acts as rank ranks[w] with its counter at counter_ptrs[w] and its own flag row at
+ * own_flag_ptrs[w] (device tables); flag_peers as above. */
+lz_status lz_peer_barrier_colocated(const unsigned long long* flag_peers, int n, const int* ranks,
+                                    int n_local, const unsigned long long* counter_ptrs,
+                                    const unsigned long long* own_flag_ptrs, void* stream);
 /* Arrival-ordered mode-0 grouped GEMM (the first expert GEMM of each direction on N > 1):
  * as lz_grouped_gemm(mode 0), but the tiles lying entirely inside self_rows[2g] ..
  * self_rows[2g+1] (the rows this rank dispatched to itself) run first, and the producer

@@ -25,6 +25,7 @@ _SIGS = {
     "lz_plan_dispatch": [_vp, _vp, _i, _i, _i, _vp, _i, _i, _i] + [_vp] * 17 + [_sz, _vp],
     "lz_set_control": [_vp],
     "lz_peer_barrier": [_vp, _i, _i, _vp, _vp, _vp],
+    "lz_peer_barrier_colocated": [_vp, _i, _vp, _i, _vp, _vp, _vp],
     "lz_pack_p2p": [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp],
     "lz_combine_p2p": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp],
     "lz_combine_bwd_p2p": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
@@ -109,7 +110,8 @@ _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
             "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1, "lz_load_record": 1,
             "lz_recovery_count": 1, "lz_pack_p2p_ret": 1, "lz_combine_bwd_p2p_ret": 1,
             "lz_grouped_gemm_scatter": 1, "lz_epoch_bump": 1, "lz_signal_peers": 1,
-            "lz_grouped_gemm_arrival": 1, "lz_peer_barrier": 1}
+            "lz_grouped_gemm_arrival": 1, "lz_peer_barrier": 1,
+            "lz_peer_barrier_colocated": 1}
 launch_count = 0
 
 

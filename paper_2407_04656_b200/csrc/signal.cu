@@ -25,12 +25,21 @@ __global__ void signal_peers_kernel(const unsigned long long* __restrict__ flag_
   }
 }
 
-// One warp: lane j publishes the new count into rank j's barrier row, then lane i waits
-// for rank i's count in ours.  Bounded by the control block (peer_wait_give_up).
+// One warp per participating rank (one warp per launch across GPUs; every co-hosted
+// rank in ONE block when several ranks share a GPU, so the waiting warps are co-resident
+// by construction): lane j publishes the new count into rank j's barrier row, then lane i
+// waits for rank i's count in ours.  Bounded by the control block (peer_wait_give_up).
 __global__ void peer_barrier_kernel(const unsigned long long* __restrict__ flag_peers, int n,
-                                    int my_rank, int* __restrict__ counter,
-                                    const int* __restrict__ own_flags) {
-  const int lane = threadIdx.x;
+                                    const int* __restrict__ ranks, int my_rank0,
+                                    const unsigned long long* __restrict__ counter_ptrs,
+                                    int* __restrict__ counter0,
+                                    const unsigned long long* __restrict__ own_flag_ptrs,
+                                    const int* __restrict__ own_flags0) {
+  const int lane = threadIdx.x % 32, w = threadIdx.x / 32;
+  const int my_rank = ranks ? ranks[w] : my_rank0;
+  int* counter = counter_ptrs ? reinterpret_cast<int*>(counter_ptrs[w]) : counter0;
+  const int* own_flags = own_flag_ptrs ? reinterpret_cast<const int*>(own_flag_ptrs[w])
+                                       : own_flags0;
   int v = 0;
   if (lane == 0) {
     v = *counter + 1;
@@ -63,8 +72,21 @@ extern "C" lz_status lz_peer_barrier(const unsigned long long* flag_peers, int n
                                      int* counter, const int* own_flags, void* stream) {
   if (!flag_peers || !counter || !own_flags || n < 1 || n > 32 || my_rank < 0 || my_rank >= n)
     return LZ_ERR_ARG;
-  peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag_peers, n, my_rank, counter,
-                                                          own_flags);
+  peer_barrier_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(flag_peers, n, nullptr, my_rank,
+                                                          nullptr, counter, nullptr, own_flags);
+  return lzh::check_launch();
+}
+
+extern "C" lz_status lz_peer_barrier_colocated(const unsigned long long* flag_peers, int n,
+                                               const int* ranks, int n_local,
+                                               const unsigned long long* counter_ptrs,
+                                               const unsigned long long* own_flag_ptrs,
+                                               void* stream) {
+  if (!flag_peers || !ranks || !counter_ptrs || !own_flag_ptrs || n < 1 || n > 32 ||
+      n_local < 1 || n_local > 32)
+    return LZ_ERR_ARG;
+  peer_barrier_kernel<<<1, 32 * n_local, 0, (cudaStream_t)stream>>>(
+      flag_peers, n, ranks, 0, counter_ptrs, nullptr, own_flag_ptrs, nullptr);
   return lzh::check_launch();
 }
 

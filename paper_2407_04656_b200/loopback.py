@@ -31,7 +31,7 @@ from __future__ import annotations
 
 import torch
 
-from . import comm
+from . import _lib, comm
 from .comm import A2A, ALLREDUCE, BARRIER, EXPERT_AR, HIST, SYMM, SYNC, WAIT
 from .layer import MoELayer, _backward_steps, _forward_steps
 
@@ -80,7 +80,7 @@ class LoopbackWorld:
         self.n = n
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.ranks = [LoopbackRank(self, r) for r in range(n)]
-        self.streams = [torch.cuda.Stream(device=self.device) for _ in range(n)]
+        self.streams = [torch.cuda.Stream(device=self.device)]   # the barrier stream
         self._alloc = None
         self.lost: set[int] = set()
         self.requests = 0
@@ -156,17 +156,29 @@ class LoopbackWorld:
         if kind == SYNC:
             return {}
         if kind == BARRIER:
-            # every rank's barrier kernel starts after ALL ranks' earlier work: on one GPU a
-            # spinning barrier CTA must never hold an SM a peer's persistent GEMM (which
-            # it waits for) still needs -- across GPUs that cannot happen
-            waits = {id(reqs[r][2]): reqs[r][2] for r in ranks}.values()
-            for r in ranks:
-                for st in waits:
-                    self.streams[r].wait_stream(st)
-                reqs[r][1].barrier(self.streams[r])
-            for r in ranks:
-                for q in ranks:
-                    reqs[r][2].wait_stream(self.streams[q])
+            # the live ranks' barriers as ONE launch (a warp per rank, lz_peer_barrier_
+            # colocated): ranks that wait on each other are never separate launches on one
+            # GPU.  It starts after every rank's earlier work (all request streams) and
+            # every request stream continues after it.
+            a = self._alloc
+            tab = torch.tensor([ranks,
+                                [a["bar"][r].data_ptr() for r in ranks],
+                                [a["flags"][r][2].data_ptr() for r in ranks]],
+                               dtype=torch.int64, device=self.device)
+            rk = tab[0].to(torch.int32)
+            waits = list({id(reqs[r][2]): reqs[r][2] for r in ranks}.values())
+            st0 = self.streams[0]
+            st0.wait_stream(torch.cuda.current_stream(self.device))
+            for st in waits:
+                st0.wait_stream(st)
+            with torch.cuda.stream(st0):
+                _lib.call("lz_peer_barrier_colocated", _lib.ptr(a["flag_peers"][2]), self.n,
+                          _lib.ptr(rk), len(ranks), _lib.ptr(tab[1]), _lib.ptr(tab[2]),
+                          st0.cuda_stream)
+                tab.record_stream(st0)
+                rk.record_stream(st0)
+            for st in waits:
+                st.wait_stream(st0)
             return {}
         if kind == SYMM:
             rows = max(reqs[r][1] for r in ranks)

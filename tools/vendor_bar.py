@@ -99,12 +99,35 @@ def run_shape(name, E, k, T, d, dff, s, out):
     # ---- weight gradient: dW2_e = dY_e^T A_e  ([d, d_ff] per expert, K = rows_e)
     dW2 = torch.empty(E, d, dff, dtype=torch.bfloat16, device=dev)
     rec("wgrad2", "lz", timeit(lambda: ops.grouped_gemm_wgrad(dY, A, off_p, dW2)), f1)
-    dYt = dYu.t().contiguous()   # [d, P]: torch's 2d x 2d form wants K (= P) contiguous in A
+    # torch's 2d x 2d (variable-K) form needs every group's K a multiple of 8 elements
+    # (16 bytes) and K contiguous in A: groups rounded up to 8 rows (zero rows, not
+    # credited), dY transposed outside the timing
+    m8 = [(v + 7) // 8 * 8 for v in m]
+    P8 = sum(m8)
+    offs8 = torch.tensor(list(torch.tensor(m8).cumsum(0)), dtype=torch.int32, device=dev)
+    dYt8 = torch.zeros(d, P8, dtype=torch.bfloat16, device=dev)
+    A8 = torch.zeros(P8, dff, dtype=torch.bfloat16, device=dev)
     try:
         rec("wgrad2", "torch._grouped_mm",
-            timeit(lambda: torch._grouped_mm(dYt, Au, offs=offs_u)), f1)
+            timeit(lambda: torch._grouped_mm(dYt8, A8, offs=offs8)), f1)
     except Exception as exc:
         res.setdefault("errors", {})["torch._grouped_mm wgrad2"] = repr(exc)[:200]
+    # lz variants with the fused epilogues (no vendor counterpart): GELU forward (writes
+    # A and the backward factor) and the dGELU backward (MN-major weights)
+    H = torch.empty(rows_p, dff, dtype=torch.bfloat16, device=dev)
+    rec("fwd1_gelu", "lz", timeit(lambda: ops.grouped_gemm_rows(X, W1, off_p, C1, aux=H,
+                                                                epilogue=_lib.LZ_EPI_GELU)), f1)
+    dH = torch.empty(rows_p, dff, dtype=torch.bfloat16, device=dev)
+    rec("dgrad1_dgelu", "lz", timeit(lambda: ops.grouped_gemm_rows(
+        dY, W2, off_p, dH, b_major=_lib.LZ_MN_MAJOR, aux=H, epilogue=_lib.LZ_EPI_DGELU)), f1)
+    dX = torch.empty(rows_p, d, dtype=torch.bfloat16, device=dev)
+    rec("dgrad2", "lz", timeit(lambda: ops.grouped_gemm_rows(dH, W1, off_p, dX,
+                                                             b_major=_lib.LZ_MN_MAJOR)), f1)
+    try:   # dX = dH . W1 with W1 [E, d_ff, d] used as [E, K=d_ff, N=d] (row-major B)
+        rec("dgrad2", "torch._grouped_mm",
+            timeit(lambda: torch._grouped_mm(dH[:P], W1, offs=offs_u)), f1)
+    except Exception as exc:
+        res.setdefault("errors", {})["torch._grouped_mm dgrad2"] = repr(exc)[:200]
     out.append(res)
     print(json.dumps(res), flush=True)
 
@@ -145,13 +168,14 @@ def run_fused_moe(out):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--json", default=None)
-    ap.add_argument("--no-fused", action="store_true")
+    ap.add_argument("--fused", action="store_true",
+                    help="also the whole-layer fused MoE forward (flashinfer JIT-compiles)")
     args = ap.parse_args()
     _lib.load()
     out = []
     run_shape("cfg2", 16, 2, 65536, 1024, 4096, 1.2, out)
     run_shape("cfg3", 8, 2, 16384, 4096, 14336, 1.2, out)
-    if not args.no_fused:
+    if args.fused:
         run_fused_moe(out)
     if args.json:
         with open(args.json, "w") as f:
