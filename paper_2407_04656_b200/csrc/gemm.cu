@@ -13,6 +13,8 @@
 // (one weight copy per (expert, rank); R[e][j] > 1 only scales capacity).
 #include <cuda.h>  // CUtensorMap (header only; the encoder is fetched at run time)
 
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "common.cuh"
@@ -390,7 +392,34 @@ struct Params {
   const int* flags;
   int n_flags;
   const int* epoch;
+  // L2-aware rasterisation: the operand slices that concurrently running tiles keep
+  // re-reading (mode 0: B = the expert's weights, one K x 256 slice per n-block; mode 1:
+  // the 256-column slices along the smaller output dimension) are visited in chunks of at
+  // most this many bytes, so a chunk stays L2-resident while the other operand streams
+  long long l2_chunk_bytes;
 };
+
+// Tile `local` of an (n_outer x n_inner) grid, ordered: for each chunk of `c` inner
+// blocks, for each outer block, for each inner block of the chunk.  c >= n_inner is the
+// plain inner-fastest order.
+__device__ __forceinline__ void chunked_raster(int local, int n_outer, int n_inner, int c, int& o,
+                                               int& i) {
+  if (c >= n_inner) {
+    o = local / n_inner;
+    i = local - o * n_inner;
+    return;
+  }
+  const int per_chunk = n_outer * c;
+  const int ch = local / per_chunk;
+  const int rem = local - ch * per_chunk;
+  const int cw = min(c, n_inner - ch * c);
+  o = rem / cw;
+  i = ch * c + (rem - o * cw);
+}
+__device__ __forceinline__ int chunk_blocks(long long budget, long long slice_bytes, int n) {
+  long long c = slice_bytes > 0 ? budget / slice_bytes : n;
+  return (int)(c < 1 ? 1 : (c > n ? n : c));
+}
 
 // Per-rank tensor maps of the scatter GEMM's return buffers ([rows, N] bf16 each): a
 // 32-row chunk whose rows return to consecutive rows of one rank (the common case: the
@@ -445,6 +474,8 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
   const int nbn = p.N / BN;
   TileInfo t;
   t.remote = false;
+  // mode 0: B slices (K x 256 weights per n-block) are the re-read operand
+  const int cb0 = p.mode == 0 ? chunk_blocks(p.l2_chunk_bytes, (long long)p.K * BN * 2, nbn) : 0;
   if (p.mode == 0 && tile < total0) {
     int acc = 0, g = 0;
     for (; g < p.G - 1; ++g) {
@@ -453,9 +484,11 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
       acc += n0;
     }
     const int local = tile - acc;
+    int mbl, nb;
+    chunked_raster(local, s_perm[g] >> 16, nbn, cb0, mbl, nb);
     t.g = g;
-    t.mb = (s_perm[g] & 0xffff) + local / nbn;
-    t.nb = local % nbn;
+    t.mb = (s_perm[g] & 0xffff) + mbl;
+    t.nb = nb;
     t.nk = p.K / BK;
     return t;
   }
@@ -467,27 +500,33 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
     else hi = mid - 1;
   }
   const int local = t1 - s_pref[lo];
-  t.nb = local % nbn;
   if (p.mode == 0) {
     t.g = lo;
-    const int mbl = local / nbn, c0 = s_perm[lo] >> 16, mlo = s_perm[lo] & 0xffff;
+    const int c0 = s_perm[lo] >> 16, mlo = s_perm[lo] & 0xffff;
+    const int nmb1 = (s_pref[lo + 1] - s_pref[lo]) / nbn;
+    int mbl, nb;
+    chunked_raster(local, nmb1, nbn, cb0, mbl, nb);
+    t.nb = nb;
     t.mb = mbl < mlo ? mbl : mbl + c0;
     t.nk = p.K / BK;
     t.remote = p.self_rows != nullptr;
   } else {
-    // weight gradient: raster along the smaller output dimension so the concurrently
-    // running tiles share the operand slices of the larger one (cfg3 dW2 = dY^T A with
-    // M = 4096, N = 14336: N-fastest order streamed A's 256-column slices from DRAM once
-    // per m-block)
+    // weight gradient: raster along the smaller output dimension (its 256-column operand
+    // slices, rows_g x 256 each, are the re-read set), in L2-sized chunks of it, so the
+    // concurrently running tiles share the slices of the larger one (cfg3 dW2 = dY^T A with
+    // M = 4096, N = 14336: N-fastest order streamed A's slices from DRAM once per m-block)
     const int nbm = p.M / C_TILE_M<CG>();
     t.g = s_perm[lo];
+    const int rows_g = s_off[t.g + 1] - s_off[t.g];
+    // (only a group with more tiles than the grid has units is visited in waves; a smaller
+    // group runs in one wave whatever its order)
+    const long long slice = nbm * nbn > (int)gridDim.x / CG ? (long long)rows_g * 256 * 2 : 0;
     if (nbm <= nbn) {
-      t.mb = local % nbm;
-      t.nb = local / nbm;
+      chunked_raster(local, nbn, nbm, chunk_blocks(p.l2_chunk_bytes, slice, nbm), t.nb, t.mb);
     } else {
-      t.mb = local / nbn;
+      chunked_raster(local, nbm, nbn, chunk_blocks(p.l2_chunk_bytes, slice, nbn), t.mb, t.nb);
     }
-    t.nk = (s_off[t.g + 1] - s_off[t.g]) / BK;
+    t.nk = rows_g / BK;
   }
   return t;
 }
@@ -1089,6 +1128,13 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 }
 
 static int g_cta_group = 2;  // default: CTA-pair kernel
+// L2 budget of the re-read operand chunk (Params::l2_chunk_bytes); LZ_GEMM_L2_CHUNK_MB
+// overrides it for A/B runs (0 = no chunking: plain inner-fastest raster)
+static long long g_l2_chunk_bytes = [] {
+  const char* e = getenv("LZ_GEMM_L2_CHUNK_MB");
+  const long long mb = e ? atoll(e) : 40;
+  return mb > 0 ? mb << 20 : (1ll << 62);
+}();
 
 LZ_DEFINE_CTL_SETTER(lz_gemm_set_control_internal)
 
@@ -1230,6 +1276,7 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
   p.flags = flags;
   p.n_flags = n_flags;
   p.epoch = epoch;
+  p.l2_chunk_bytes = g_l2_chunk_bytes;
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (sms < 2) sms = 2;

@@ -32,11 +32,25 @@ def rel(got, ref):
     return float((got - ref).norm() / ref.norm().clamp_min(1e-12))
 
 
-def check(layer, group, Tn, seed, tag):
+def _gather_rows(t, group, sizes):
+    """all-gather of per-rank row blocks of different lengths (padded to the max)."""
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    pad[:t.shape[0]] = t
+    out = [torch.empty_like(pad) for _ in sizes]
+    dist.all_gather(out, pad, group=group)
+    return [o[:sz] for o, sz in zip(out, sizes)]
+
+
+def check(layer, group, Tn, seed, tag, ragged=False):
+    """ragged: every rank routes a different number of tokens (Tn + 96 * rank) -- the
+    reference allows arbitrary per-rank counts T[e][j]."""
     rank, n = dist.get_rank(group), dist.get_world_size(group)
     dev = torch.device("cuda", torch.cuda.current_device())
     g = torch.Generator(device=dev)
     g.manual_seed(seed + rank)
+    sizes = [Tn + (96 * r if ragged else 0) for r in range(n)]
+    Tn = sizes[rank]
     x = torch.randn(Tn, layer.d, generator=g, device=dev).bfloat16().requires_grad_(True)
     dout = torch.randn(Tn, layer.d, generator=g, device=dev).bfloat16()
     layer.zero_grad(set_to_none=True)
@@ -47,12 +61,9 @@ def check(layer, group, Tn, seed, tag):
     k, E = layer.k, layer.E
     gidx = ops.router_gate(x.detach(), layer.wg.detach(), layer.bg.detach(), k)[0]
     # gather the global batch on every rank
-    xs = [torch.empty_like(x.detach()) for _ in range(n)]
-    ds = [torch.empty_like(dout) for _ in range(n)]
-    ids = [torch.empty_like(gidx) for _ in range(n)]
-    dist.all_gather(xs, x.detach().contiguous(), group=group)
-    dist.all_gather(ds, dout, group=group)
-    dist.all_gather(ids, gidx, group=group)
+    xs = _gather_rows(x.detach().contiguous(), group, sizes)
+    ds = _gather_rows(dout, group, sizes)
+    ids = _gather_rows(gidx, group, sizes)
     # full weights: every owner holds the deterministic per-expert init (no optimizer step)
     from paper_2407_04656_b200.layer import _expert_weights
     w1 = torch.stack([_expert_weights(layer.seed, 2 * e, (layer.d_ff, layer.d), layer.init_std, dev)
@@ -67,7 +78,7 @@ def check(layer, group, Tn, seed, tag):
     ref, _, _, _ = moe_ref.moe_forward_ref(X, wg, bg, w1, w2, k, layer.renorm,
                                            idx=torch.cat([t.cpu() for t in ids]))
     ref.backward(torch.cat([t.float().cpu() for t in ds]))
-    sl = slice(rank * Tn, (rank + 1) * Tn)
+    sl = slice(sum(sizes[:rank]), sum(sizes[:rank + 1]))
     errs = {"out": rel(out, ref[sl]), "dx": rel(x.grad, X.grad[sl]), "dwg": rel(layer.wg.grad, wg.grad),
             "dbg": rel(layer.bg.grad, bg.grad)}
     for p, e in enumerate(layer.local_ids):
@@ -77,6 +88,55 @@ def check(layer, group, Tn, seed, tag):
     print(f"[{tag}] rank {rank}/{n} local experts {layer.local_ids} imbalance "
           f"{layer.imbalance():.3f} max rel err {max(errs.values()):.3e}", flush=True)
     assert not bad, f"rank {rank}: {bad}"
+
+
+def kill_mid_step(layer, group, Tn, loads, c):
+    """A rank dies mid-step -- after the histogram all-gather and its dispatch, before
+    its expert GEMMs and the combine.  The survivors' device waits (arrival
+    flags, peer barrier) give up after the control block's timeout instead of hanging,
+    check() raises StepAbortedError, the step is discarded, and the survivors shrink the
+    communicator, re-plan with the reference recipe, move the expert state and resume."""
+    from paper_2407_04656_b200 import _lib, comm
+    from paper_2407_04656_b200.elastic import shrink_and_replan
+    from paper_2407_04656_b200.layer import StepAbortedError
+    cur = dist.get_world_size(group)
+    me = dist.get_rank(group)
+    victim = cur - 1
+    _lib.control(timeout_s=3.0)
+    _lib.control_reset()
+    dist.barrier(group=group)
+    torch.cuda.synchronize()
+
+    class Dying(comm.ProcessFabric):
+        def serve(self, req):
+            if req[0] == comm.SYNC:          # after this rank's dispatch + arrival signal
+                torch.cuda.synchronize()
+                print(f"rank {dist.get_rank()} dies mid-step", flush=True)
+                os._exit(0)
+            return super().serve(req)
+
+    if me == victim:
+        fab = Dying(group)
+        layer.fabric = fab
+    g = torch.Generator(device="cuda")
+    g.manual_seed(5)
+    x = torch.randn(Tn, layer.d, generator=g, device="cuda").bfloat16()
+    with torch.no_grad():
+        layer(x)
+    torch.cuda.synchronize()
+    try:
+        layer.check()
+        raise AssertionError("a lost peer must abort the step")
+    except StepAbortedError as exc:
+        print(f"rank {dist.get_rank()} step aborted: {exc.status}", flush=True)
+    _lib.control_reset()
+    _lib.control(timeout_s=10.0)
+    opt = torch.optim.Adam([layer.w1, layer.w2], lr=1e-4)
+    layer, group, rep = shrink_and_replan(layer, group, [victim], loads, c, optimizer=opt)
+    if dist.get_rank(group) == 0:
+        print(f"re-plan after mid-step loss: {rep}", flush=True)
+    check(layer, group, Tn, 400, f"N={dist.get_world_size(group)} after mid-step loss")
+    return layer, group
 
 
 def main():
@@ -93,6 +153,7 @@ def main():
     layer = MoELayer(d, dff, E, k, replicas=R, group=dist.group.WORLD, seed=7, init_std=0.05,
                      router_bias=bias)
     check(layer, dist.group.WORLD, Tn, 100, f"N={n}")
+    check(layer, dist.group.WORLD, Tn, 150, f"N={n} ragged batches", ragged=True)
     group = dist.group.WORLD
     if "--rebalance" in sys.argv:
         # the routing skew moves (new hot experts): the device load window sees it and the
@@ -123,10 +184,14 @@ def main():
             if dist.get_rank(group) in exclude:
                 print(f"rank {rank} leaves (simulated failure)", flush=True)
                 os._exit(0)
-            layer, group, rep = shrink_and_replan(layer, group, exclude, loads, c)
+            opt = torch.optim.Adam([layer.w1, layer.w2], lr=1e-4)
+            layer, group, rep = shrink_and_replan(layer, group, exclude, loads, c, optimizer=opt)
+            assert opt.param_groups[0]["params"][0] is layer.w1
             if dist.get_rank(group) == 0:
                 print(f"re-plan: {rep}", flush=True)
             check(layer, group, Tn, 200 + cur, f"N={dist.get_world_size(group)} after failure")
+    if "--kill" in sys.argv and dist.get_world_size(group) >= 2:
+        layer, group = kill_mid_step(layer, group, Tn, loads, c)
     dist.barrier(group=group)
     if dist.get_rank(group) == 0:
         print("DIST OK", flush=True)

@@ -26,6 +26,8 @@ def test_dist_layer(env):
            os.path.join(ROOT, "tests", "dist_layer_check.py"), "--rebalance"]
     if n > 2 and not env:
         cmd.append("--elastic")
+    if not env:
+        cmd.append("--kill")
     r = subprocess.run(cmd, env={**os.environ, **env}, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "DIST OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
