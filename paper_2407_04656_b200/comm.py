@@ -147,10 +147,7 @@ class ReplicaGroups:
                 key = (parent, tuple(base[j] for j in s), backend, max_ctas)
                 pg = _PG_CACHE.get(key)
                 if pg is None:
-                    # members-only synchronisation: ranks lost to a failure (still in the
-                    # default group) never enter this call
-                    pg = dist.new_group([base[j] for j in s], backend=backend, pg_options=opts,
-                                        use_local_synchronization=True)
+                    pg = dist.new_group([base[j] for j in s], backend=backend, pg_options=opts)
                     _PG_CACHE[key] = pg
                 if self.rank in s:
                     self.groups[s] = pg
