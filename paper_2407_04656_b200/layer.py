@@ -134,6 +134,7 @@ class MoELayer(torch.nn.Module):
         # stream while the two weight-gradient GEMMs run (they fill the GEMM tails; cfg2
         # graph replay 6.12 -> 6.04 ms/step at N = 1, tools/tail_ab.py)
         self.tail_overlap = os.environ.get("LZ_TAIL_OVERLAP", "1") != "0"
+        self.tail_overlap_nx = os.environ.get("LZ_TAIL_OVERLAP_NX", "0") == "1"   # N > 1
         self._tail_stream = None
         # exchange buffers: rows = slack x this rank's assignments (+ expert padding); the
         # planner detects a larger need on the device and reserve() grows them
@@ -479,10 +480,12 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
     # the GEMMs next to them leave `overlap_reserve` SMs free
     ov = max(2, (lzh_num_sms() - layer.overlap_reserve)) if N > 1 else 0
     main = torch.cuda.current_stream(dev)
-    # tail overlap: dX GEMM right after the dgrad GEMM; the dispatch backward + router
-    # weight gradient (they need only dX, dw and the gate state) then run on a side
-    # stream under the two weight-gradient GEMMs (and, N > 1, their all-reduces)
-    tail = layer.tail_overlap and mode in ("local", "p2p") and (mode == "local" or scatter)
+    # tail overlap (N = 1): dX GEMM right after the dgrad GEMM; the dispatch backward +
+    # router weight gradient (they need only dX, dw and the gate state) then run on a side
+    # stream under the two weight-gradient GEMMs.  N > 1 keeps the dX GEMM last: it hides
+    # the all-reduce of the last expert gradient (~0.33 ms at cfg2, N = 2), which the tail
+    # overlap would expose instead (measured 6.57 vs ~6.1 ms/step at N = 2).
+    tail = layer.tail_overlap and (mode == "local" or (scatter and layer.tail_overlap_nx))
     if G > 0:
         # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H); on N > 1 the
         # tiles of our own rows start while the other ranks' dY rows arrive
