@@ -392,10 +392,11 @@ struct Params {
   const int* flags;
   int n_flags;
   const int* epoch;
-  // L2-aware rasterisation: the operand slices that concurrently running tiles keep
-  // re-reading (mode 0: B = the expert's weights, one K x 256 slice per n-block; mode 1:
-  // the 256-column slices along the smaller output dimension) are visited in chunks of at
-  // most this many bytes, so a chunk stays L2-resident while the other operand streams
+  // L2-aware rasterisation of the row GEMMs (mode 0): the expert's weight slices (K x 256
+  // per n-block) that concurrently running tiles re-read are visited in chunks of at most
+  // this many bytes, so a chunk stays L2-resident while the token rows stream (cfg3
+  // W1|W3 is 235 MB per expert: n-fastest order re-read it from DRAM for every m-block,
+  // 27 GB per launch)
   long long l2_chunk_bytes;
 };
 
@@ -511,20 +512,18 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
     t.nk = p.K / BK;
     t.remote = p.self_rows != nullptr;
   } else {
-    // weight gradient: raster along the smaller output dimension (its 256-column operand
-    // slices, rows_g x 256 each, are the re-read set), in L2-sized chunks of it, so the
-    // concurrently running tiles share the slices of the larger one (cfg3 dW2 = dY^T A with
-    // M = 4096, N = 14336: N-fastest order streamed A's slices from DRAM once per m-block)
+    // weight gradient: raster along the smaller output dimension so the concurrently
+    // running tiles share the operand slices of the larger one (cfg3 dW2 = dY^T A with
+    // M = 4096, N = 14336: N-fastest order streamed A's 256-column slices from DRAM once
+    // per m-block).  No chunking here: the slices along the smaller dimension are the
+    // few ones, and chunking them re-reads the many ones (cfg3 dW1: 2.7x the 1.9 GB dH)
     const int nbm = p.M / C_TILE_M<CG>();
     t.g = s_perm[lo];
     const int rows_g = s_off[t.g + 1] - s_off[t.g];
-    // (only a group with more tiles than the grid has units is visited in waves; a smaller
-    // group runs in one wave whatever its order)
-    const long long slice = nbm * nbn > (int)gridDim.x / CG ? (long long)rows_g * 256 * 2 : 0;
     if (nbm <= nbn) {
-      chunked_raster(local, nbn, nbm, chunk_blocks(p.l2_chunk_bytes, slice, nbm), t.nb, t.mb);
+      chunked_raster(local, nbn, nbm, nbm, t.nb, t.mb);
     } else {
-      chunked_raster(local, nbm, nbn, chunk_blocks(p.l2_chunk_bytes, slice, nbn), t.mb, t.nb);
+      chunked_raster(local, nbm, nbn, nbn, t.mb, t.nb);
     }
     t.nk = rows_g / BK;
   }
