@@ -611,11 +611,12 @@ def run_gpu(args, cfg):
 
 def isolated_hbm_kernels(layer, x, dout, hbm, reps=20):
     """Each HBM-bound kernel of the step replayed `reps` times back to back on the step's
-    own shapes and routing (one CUDA-event pair around the loop, so host launch gaps are
-    hidden behind the queue, unlike the eager stage marks).  The working set of every
-    launch (>= 400 MB, except the gate's 134 MB of x) exceeds the 126 MB L2, and the
-    kernels alternate between two input copies so no launch re-reads the previous
-    launch's input from L2.  Bytes are the algorithmic ones of SURVEY.md 8d."""
+    own shapes and routing: the `reps` launches are captured in ONE CUDA graph whose replay
+    is timed with a CUDA-event pair, so neither host launch gaps nor the wrappers' output
+    allocations are inside the timed region.  The working set of every launch (>= 400 MB,
+    except the gate's 134 MB of x) exceeds the 126 MB L2, and the kernels alternate
+    between two input copies so no launch re-reads the previous launch's input from L2.
+    Bytes are the algorithmic ones of SURVEY.md 8d."""
     from paper_2407_04656_b200 import ops
     from paper_2407_04656_b200.dispatch import plan_device
 
@@ -657,15 +658,26 @@ def isolated_hbm_kernels(layer, x, dout, hbm, reps=20):
     }
     out = {}
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    side = torch.cuda.Stream(device=x.device)
     for name, (fn, nbytes) in kernels.items():
         for i in range(4):
             fn(i & 1)
         torch.cuda.synchronize()
+        # the `reps` launches captured in ONE CUDA graph and replayed: the wrappers' host
+        # work (output allocation, ctypes) is outside the timed region, which then holds
+        # only the kernels, back to back
+        side.wait_stream(torch.cuda.current_stream(x.device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            for i in range(reps):
+                fn(i & 1)
+        g.replay()
+        torch.cuda.synchronize()
         ev0.record()
-        for i in range(reps):
-            fn(i & 1)
+        g.replay()
         ev1.record()
         torch.cuda.synchronize()
+        del g
         us = ev0.elapsed_time(ev1) / reps * 1e3
         gbs = nbytes / (us * 1e-6) / 1e9
         out[name] = {"MB": round(nbytes / 1e6, 1), "us": round(us, 1), "GBps": round(gbs, 1),
