@@ -132,7 +132,9 @@ def kill_mid_step(layer, group, Tn, loads, c):
     _lib.control_reset()
     _lib.control(timeout_s=10.0)
     opt = torch.optim.Adam([layer.w1, layer.w2], lr=1e-4)
-    layer, group, rep = shrink_and_replan(layer, group, [victim], loads, c, optimizer=opt)
+    # the survivors need slots for every expert (f_eff drops with the node count)
+    slots = max(c, math.ceil(layer.E / (cur - 1)))
+    layer, group, rep = shrink_and_replan(layer, group, [victim], loads, slots, optimizer=opt)
     if dist.get_rank(group) == 0:
         print(f"re-plan after mid-step loss: {rep}", flush=True)
     check(layer, group, Tn, 400, f"N={dist.get_world_size(group)} after mid-step loss")
@@ -184,9 +186,14 @@ def main():
             if dist.get_rank(group) in exclude:
                 print(f"rank {rank} leaves (simulated failure)", flush=True)
                 os._exit(0)
-            opt = torch.optim.Adam([layer.w1, layer.w2], lr=1e-4)
+            # lr = 0: Adam's moments are populated from the last check's gradients while
+            # the weights keep their deterministic values (check() rebuilds them)
+            opt = torch.optim.Adam([layer.w1, layer.w2], lr=0.0)
+            opt.step()
             layer, group, rep = shrink_and_replan(layer, group, exclude, loads, c, optimizer=opt)
             assert opt.param_groups[0]["params"][0] is layer.w1
+            assert rep["optimizer_state_keys"] == ["exp_avg", "exp_avg_sq"], rep
+            assert opt.state[layer.w1]["exp_avg"].shape[0] == len(layer.local_ids)
             if dist.get_rank(group) == 0:
                 print(f"re-plan: {rep}", flush=True)
             check(layer, group, Tn, 200 + cur, f"N={dist.get_world_size(group)} after failure")
