@@ -3,6 +3,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 #include "../../include/lz.h"
 
@@ -121,6 +124,16 @@ __device__ __forceinline__ bool peer_wait_give_up(long long& deadline) {
   return false;
 }
 
+// ---- programmatic dependent launch (PDL) ------------------------------------------------
+// Kernels of the step's chain are launched with programmatic stream serialisation
+// (lzh::launch): each lets its dependents launch as soon as all of its blocks are running
+// and waits for its own predecessor's completion (and memory) before touching its
+// outputs, so a kernel's launch and prologue overlap the previous kernel's tail.
+__device__ __forceinline__ void pdl_prologue() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -142,6 +155,40 @@ inline lz_status check_launch() {
     return LZ_ERR_CUDA;
   }
   return LZ_OK;
+}
+inline bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("LZ_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0;
+}
+// cudaLaunchKernelEx with programmatic stream serialisation (see pdl_prologue) and an
+// optional cluster size; every kernel launched this way calls pdl_prologue() first.
+template <typename... KArgs, typename... Args>
+inline lz_status launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                        cudaStream_t s, int cluster, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  ++na;
+  if (cluster > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = cluster;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+  return check_launch();
 }
 inline int num_sms() {
   static int n = 0;

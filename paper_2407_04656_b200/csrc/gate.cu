@@ -500,6 +500,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
   __shared__ __align__(8) uint64_t full_bar[kGsStages], empty_bar[kGsStages];
   __shared__ __align__(8) uint64_t tfull_bar[kGsTiles], tempty_bar[kGsTiles];
   __shared__ int32_t s_hist[16];
+  pdl_prologue();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int rowb = (d + 8) * 2;                    // padded smem row, bytes
   uint8_t* ring = gs_smem;                         // [stages][16][d + 8] bf16
@@ -693,7 +694,20 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
     const size_t smem = gs_smem_bytes(d);
     const int ngroups = (Tn + 15) / 16;
     const int sgrid = ngroups < lzh::num_sms() ? ngroups : lzh::num_sms();
-#define LZ_ROUTER_STREAM(n)                                                                    case n: {                                                                                      static bool attr = false;                                                                    if (!attr) {                                                                                   if (cudaFuncSetAttribute(router_gate_stream<n>,                                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,                                                 (int)gs_smem_bytes(1024)) != cudaSuccess)                             return lzh::check_launch();                                                                attr = true;                                                                               }                                                                                            router_gate_stream<n><<<sgrid, kGsThreads, smem, s>>>(xb, wb, bias, Tn, d, E, k,                                                                    renorm, idx, w, probs,                                                                       hist);                        break;                                                                                     }
+#define LZ_ROUTER_STREAM(n)                                                                 \
+  case n: {                                                                                 \
+    static bool attr = false;                                                               \
+    if (!attr) {                                                                            \
+      if (cudaFuncSetAttribute(router_gate_stream<n>,                                       \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                               (int)gs_smem_bytes(1024)) != cudaSuccess)                    \
+        return lzh::check_launch();                                                         \
+      attr = true;                                                                          \
+    }                                                                                       \
+    lzh::launch(router_gate_stream<n>, dim3(sgrid), dim3(kGsThreads), smem, s, 1, xb, wb,  \
+                bias, Tn, d, E, k, renorm, idx, w, probs, hist);                            \
+    break;                                                                                  \
+  }
     switch (NT) {
       LZ_ROUTER_STREAM(1)
       LZ_ROUTER_STREAM(2)

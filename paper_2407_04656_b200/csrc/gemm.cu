@@ -748,6 +748,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
+  pdl_prologue();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t cta = CG == 1 ? 0u : cluster_ctarank();
   const bool leader = cta == 0;
@@ -1160,13 +1161,15 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = Cfg<CG, AUX>::kSmemBytes;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;   // pdl_prologue
+  attr[1].val.programmaticStreamSerializationAllowed = lzh::pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, p, rm) != cudaSuccess)
     return lzh::check_launch();
   return lzh::check_launch();

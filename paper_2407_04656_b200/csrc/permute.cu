@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(kRowThreads) pack_kernel(
     const unsigned long long* __restrict__ ret_peers, long long* __restrict__ ret_own,
     int my_rank, const int32_t* __restrict__ ret_row) {
   const int lane = threadIdx.x % 32;
+  pdl_prologue();
   const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
   const long nw = (long)gridDim.x * kRowWarps;
   const int nch = d / 8;
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(
     const unsigned long long* __restrict__ peers, const float* __restrict__ w, int Tn, int d, int k,
     uint4* __restrict__ out) {
   const int lane = threadIdx.x % 32;
+  pdl_prologue();
   const long gw = (long)blockIdx.x * kRowWarps + threadIdx.x / 32;
   const long nw = (long)gridDim.x * kRowWarps;
   const int nch = d / 8;
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
     float* __restrict__ dw, int E, const int32_t* __restrict__ recv_m,
     const int32_t* __restrict__ recv_off, long n_pad_items,
     const int32_t* __restrict__ yrow) {
+  pdl_prologue();
   // yrow (optional): y is this rank's own return buffer and assignment p's expert output
   // sits at row yrow[p] (written by the owners' scattering GEMM epilogue); dy still goes
   // to the owner's row
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(32 * kDWarps) dispatch_bwd_kernel(
   __shared__ __align__(16) float s_dl[kDWarps][64][kDT + 1];    // [expert][token]
   __shared__ __align__(16) float s_rt[kDWarps][kDT][64 + 4];    // router term, one pass
   __shared__ long long s_src[kDWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
+  pdl_prologue();
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const long gw = (long)blockIdx.x * kDWarps + warp;
   const long nw = (long)gridDim.x * kDWarps;
@@ -486,6 +490,7 @@ __global__ void __launch_bounds__(128, 2) router_wgrad_tc(const float* __restric
                                                        float* __restrict__ part,
                                                        float* __restrict__ part_bias) {
   extern __shared__ __align__(16) uint8_t rw_smem[];
+  pdl_prologue();
   __nv_bfloat16* s_x = reinterpret_cast<__nv_bfloat16*>(rw_smem);  // [stages][16][kRwRow]
   float* s_dl = reinterpret_cast<float*>(rw_smem + kRwStages * kRwTok * kRwRow * 2);
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
@@ -621,6 +626,7 @@ __global__ void __launch_bounds__(256) router_wgrad_reduce(const float* __restri
                                                            float* __restrict__ dwg,
                                                            float* __restrict__ dbias) {
   __shared__ float s_sum[8][33];
+  pdl_prologue();
   const long n = (long)E * d;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long nmain = (n + 31) / 32;
@@ -702,10 +708,9 @@ static lz_status pack_impl(const void* x, int Tn, int d, int k, const int32_t* r
   if (E > 0 && (!recv_m || !recv_off || !out)) return LZ_ERR_ARG;
   const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
   if (Tn + npad == 0) return LZ_OK;
-  pack_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)x, Tn, d, k, row, prank, peers, (uint4*)out, E, recv_m, recv_off, npad,
-      ret_peers, ret_own, my_rank, ret_row);
-  return lzh::check_launch();
+  return lzh::launch(pack_kernel, dim3(row_grid(Tn + npad)), dim3(kRowThreads), 0,
+                     (cudaStream_t)stream, 1, (const uint4*)x, Tn, d, k, row, prank, peers,
+                     (uint4*)out, E, recv_m, recv_off, npad, ret_peers, ret_own, my_rank, ret_row);
 }
 
 extern "C" lz_status lz_pack(const void* x, int Tn, int d, int k, const int32_t* row, void* out,
@@ -740,9 +745,9 @@ static lz_status combine_impl(const void* y, const int32_t* row, const int32_t* 
   if (Tn < 0 || d <= 0 || d % 8 || k < 1 || k > LZ_MAX_TOPK) return LZ_ERR_ARG;
   if (Tn == 0) return LZ_OK;
   if ((!y && !peers) || !row || !w || !out) return LZ_ERR_ARG;
-  combine_kernel<<<row_grid(Tn), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)y, row, prank, peers, w, Tn, d, k, (uint4*)out);
-  return lzh::check_launch();
+  return lzh::launch(combine_kernel, dim3(row_grid(Tn)), dim3(kRowThreads), 0,
+                     (cudaStream_t)stream, 1, (const uint4*)y, row, prank, peers, w, Tn, d, k,
+                     (uint4*)out);
 }
 
 extern "C" lz_status lz_combine(const void* y, const int32_t* row, const float* w, int Tn, int d,
@@ -769,10 +774,10 @@ static lz_status combine_bwd_impl(const void* dout, const void* y, const int32_t
   if (E > 0 && (!recv_m || !recv_off || !dy)) return LZ_ERR_ARG;
   const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
   if (Tn + npad == 0) return LZ_OK;
-  combine_bwd_kernel<<<row_grid(Tn + npad), kRowThreads, 0, (cudaStream_t)stream>>>(
-      (const uint4*)dout, (const uint4*)y, row, prank, peers_y, peers_dy, w, Tn, d, k, (uint4*)dy,
-      dw, E, recv_m, recv_off, npad, yrow);
-  return lzh::check_launch();
+  return lzh::launch(combine_bwd_kernel, dim3(row_grid(Tn + npad)), dim3(kRowThreads), 0,
+                     (cudaStream_t)stream, 1, (const uint4*)dout, (const uint4*)y, row, prank,
+                     peers_y, peers_dy, w, Tn, d, k, (uint4*)dy, dw, E, recv_m, recv_off, npad,
+                     yrow);
 }
 
 extern "C" lz_status lz_combine_bwd(const void* dout, const void* y, const int32_t* row,
@@ -821,9 +826,9 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
   const long dcap = (long)lzh::num_sms() * 16;
   if (dgrid > dcap) dgrid = dcap;
 #define LZ_DBWD(ks)                                                                          \
-  dispatch_bwd_kernel<ks><<<(int)dgrid, 32 * kDWarps, 0, (cudaStream_t)stream>>>(              \
-      (const uint4*)dxe, row, prank, peers, Tn, d, k, probs, idx, dw, (const __nv_bfloat16*)wg, \
-      E, renorm, (uint4*)dx, dlogits)
+  lzh::launch(dispatch_bwd_kernel<ks>, dim3((int)dgrid), dim3(32 * kDWarps), 0,                 \
+              (cudaStream_t)stream, 1, (const uint4*)dxe, row, prank, peers, Tn, d, k, probs,   \
+              idx, dw, (const __nv_bfloat16*)wg, E, renorm, (uint4*)dx, dlogits)
   switch ((E + 15) / 16) {
     case 1: LZ_DBWD(1); break;
     case 2: LZ_DBWD(2); break;
@@ -899,8 +904,8 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
       attr = true;
     }
     dim3 grid(nblk, (d + kRwCols - 1) / kRwCols, (E + 15) / 16);
-    router_wgrad_tc<<<grid, 128, kRwSmem, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
-                                               part_bias);
+    lzh::launch(router_wgrad_tc, grid, dim3(128), kRwSmem, s, 1, dlogits,
+                (const __nv_bfloat16*)x, Tn, d, E, part, part_bias);
   } else {
     dim3 grid(nblk, (d + 1023) / 1024, (E + kWgE - 1) / kWgE);
     router_wgrad_partial<<<grid, 256, 0, s>>>(dlogits, (const __nv_bfloat16*)x, Tn, d, E, part,
@@ -909,9 +914,8 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
   lz_status st = lzh::check_launch();
   if (st != LZ_OK) return st;
   const long n = (long)E * d;
-  router_wgrad_reduce<<<(int)((n + 31) / 32 + (E + 31) / 32), 256, 0, s>>>(part, part_bias, nblk,
-                                                                          d, E, dwg, dbias);
-  return lzh::check_launch();
+  return lzh::launch(router_wgrad_reduce, dim3((int)((n + 31) / 32 + (E + 31) / 32)), dim3(256),
+                     0, s, 1, (const float*)part, (const float*)part_bias, nblk, d, E, dwg, dbias);
 }
 
 extern "C" lz_status lz_copy_segments(const void* in, void* out, int d, int nseg,

@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(kSlotThreads) count_kernel(const int32_t* __re
                                                              int32_t* __restrict__ blk_counts,
                                                              int32_t* __restrict__ err) {
   extern __shared__ int32_t s_hist[];
+  pdl_prologue();
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   __syncthreads();
   const int b = blockIdx.x;
@@ -162,6 +163,7 @@ struct PlanArgs {
 // shared memory instead of re-reading its own global writes)
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char s_raw[];
+  pdl_prologue();
   const int E = a.E, N = a.N, rank = a.rank;
   int64_t* s_q = reinterpret_cast<int64_t*>(s_raw);
   int32_t* s_M = reinterpret_cast<int32_t*>(s_q + E);  // M[j][e] = sum_i D[i][e][j]
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(kSlotThreads) slot_kernel(
     int32_t* __restrict__ slot, int32_t* __restrict__ gather, int32_t* __restrict__ dest_row,
     int32_t* __restrict__ dest_rank, int32_t* __restrict__ err, int rank, int cap_rows) {
   extern __shared__ int32_t s_cnt[];  // [kSlotWarps][E]
+  pdl_prologue();
   const int b = blockIdx.x;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (cap_rows > 0 && (*(volatile int32_t*)err & LZ_ERRF_CAPACITY)) {
@@ -441,24 +444,23 @@ extern "C" lz_status lz_plan_dispatch(const int32_t* T, const int32_t* R, int E,
   int32_t* sdelta = (int32_t*)w;      w += align_up(sizeof(int32_t) * E * N, 256);
   int32_t* ddelta = (int32_t*)w;
 
-  if (P > 0) {
-    count_kernel<<<B, kSlotThreads, sizeof(int32_t) * E, s>>>(routed, P, E, B, blk_counts, err);
-    if ((st = lzh::check_launch()) != LZ_OK) return st;
-  }
+  if (P > 0 && (st = lzh::launch(count_kernel, dim3(B), dim3(kSlotThreads), sizeof(int32_t) * E,
+                                 s, 1, routed, P, E, B, blk_counts, err)) != LZ_OK)
+    return st;
   PlanArgs a{T, R, E, N, rank, align, P, B, quota, D, send_sizes, recv_sizes, recv_counts,
              recv_m, recv_off, recv_src_off, recv_stage_off, recv_cnt, err, blk_counts,
              blk_base, pref, sdelta, ddelta, plan_d_smem(E, N) ? 1 : 0, cap_rows, need_rows};
   const size_t smem = plan_smem(E, N, a.d_smem != 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  plan_kernel<<<1, kPlanThreads, smem, s>>>(a);
-  if ((st = lzh::check_launch()) != LZ_OK) return st;
-  if (P > 0) {
-    slot_kernel<<<B, kSlotThreads, sizeof(int32_t) * kSlotWarps * E, s>>>(
-        routed, P, E, N, B, blk_base, pref, sdelta, ddelta, slot, gather, dest_row, dest_rank, err,
-        rank, cap_rows);
-    if ((st = lzh::check_launch()) != LZ_OK) return st;
-  }
+  if ((st = lzh::launch(plan_kernel, dim3(1), dim3(kPlanThreads), smem, s, 1, a)) != LZ_OK)
+    return st;
+  if (P > 0)
+    return lzh::launch(slot_kernel, dim3(B), dim3(kSlotThreads),
+                       sizeof(int32_t) * kSlotWarps * E, s, 1, routed, P, E, N, B,
+                       (const int32_t*)blk_base, (const int32_t*)pref, (const int32_t*)sdelta,
+                       (const int32_t*)ddelta, slot, gather, dest_row, dest_rank, err, rank,
+                       cap_rows);
   return LZ_OK;
 }
 
