@@ -90,6 +90,37 @@ def check(layer, group, Tn, seed, tag, ragged=False):
     assert not bad, f"rank {rank}: {bad}"
 
 
+def multilayer(group, n_layers=4):
+    """A stack of cfg2-sized layers (E16 top-2, d1024, d_ff4096, 65,536 tokens per rank):
+    the plan-sized exchange buffers (1.25 x the balanced share, not N x Tn x k) keep a
+    multi-layer step within HBM; one fwd + bwd through all layers, peak memory reported."""
+    n = dist.get_world_size(group)
+    E, k, d, dff, Tn = 16, 2, 1024, 4096, 65536
+    bias = zipf_router_bias(E, 1.2, seed=0)
+    loads = (torch.softmax(bias, 0) * Tn * n * k).round().long().clamp_min(1).tolist()
+    R = replica_matrix(plan_for_loads(loads, n, math.ceil(6 * E / n), 2))
+    layers = [MoELayer(d, dff, E, k, replicas=R, group=group, seed=li, router_bias=bias,
+                       router_std=1.28 / math.sqrt(d)) for li in range(n_layers)]
+    torch.cuda.reset_peak_memory_stats()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(dist.get_rank(group))
+    x = torch.randn(Tn, d, generator=g, device="cuda").bfloat16().requires_grad_(True)
+    h = x
+    for L in layers:
+        h = L(h)
+    h.float().square().mean().backward()
+    torch.cuda.synchronize()
+    for L in layers:
+        L.check()
+    peak = torch.cuda.max_memory_allocated() / 2**30
+    rows = layers[0]._symm.rows
+    print(f"[{n_layers} layers N={n}] rank {dist.get_rank(group)} exchange rows {rows} "
+          f"(N*Tn*k = {n * Tn * k}), peak memory {peak:.1f} GiB, "
+          f"dx finite {bool(torch.isfinite(x.grad.float()).all())}", flush=True)
+    assert torch.isfinite(x.grad.float()).all()
+    del layers, h, x
+
+
 def kill_mid_step(layer, group, Tn, loads, c):
     """A rank dies mid-step -- after the histogram all-gather and its dispatch, before
     its expert GEMMs and the combine.  The survivors' device waits (arrival
@@ -197,6 +228,8 @@ def main():
             if dist.get_rank(group) == 0:
                 print(f"re-plan: {rep}", flush=True)
             check(layer, group, Tn, 200 + cur, f"N={dist.get_world_size(group)} after failure")
+    if "--multilayer" in sys.argv:
+        multilayer(group)
     if "--kill" in sys.argv and dist.get_world_size(group) >= 2:
         layer, group = kill_mid_step(layer, group, Tn, loads, c)
     dist.barrier(group=group)

@@ -345,3 +345,45 @@ def test_loopback_full_size_cfg3_sampled():
         ref.backward(douts[r][samples[r]].float().cpu())
         _rel(outs[r][samples[r]], ref, name=f"rank {r} out")
         _rel(grads[r][0][samples[r]], xr.grad, name=f"rank {r} dx")
+
+
+def test_loopback_elastic_8_6_4():
+    """BASELINE cfg5's 8 -> 6 -> 4 reconfiguration on one GPU: 8 virtual ranks, two ranks
+    lost mid-step (after their dispatch), shrink to 6 with the reference re-plan recipe and
+    expert-state moves, then two more lost, shrink to 4; after each shrink a full fwd + bwd
+    step matches the oracle.  Slots per rank stay at the 8-rank value."""
+    from paper_2407_04656_b200 import _lib
+    from paper_2407_04656_b200.layer import StepAbortedError
+    N, E, k, d, dff, Tn = 8, 16, 2, 512, 1024, 512
+    slots = math.ceil(6 * E / 8)
+    world, layers, R = _world(N, E, k, d, dff, "gelu", 1.2, slot_factor=6)
+    xs, douts = _inputs(N, Tn, d)
+    loads = [int(1000 / (e + 1) ** 1.2) + 1 for e in range(E)]
+    _lib.control(timeout_s=0.25)
+    _lib.control_reset()
+    try:
+        world.step(layers, xs, douts)
+        torch.cuda.synchronize()
+        for L in layers:
+            L.check()
+        for lost in ((3, 6), (1, 4)):
+            world.step(layers, xs, lose={r: 2 for r in lost})   # after their dispatch
+            torch.cuda.synchronize()
+            assert world.lost == set(lost)
+            for r, L in enumerate(layers):
+                if r not in lost:
+                    with pytest.raises(StepAbortedError):
+                        L.check()
+            _lib.control_reset()
+            world, layers, report = world.shrink(layers, loads, slots=slots)
+            keep = report["live"]
+            xs, douts = [xs[r] for r in keep], [douts[r] for r in keep]
+            outs, grads = world.step(layers, xs, douts)
+            torch.cuda.synchronize()
+            for L in layers:
+                L.check()
+            _check_against_oracle(world, layers, xs, douts, outs, grads)
+        assert world.n == 4
+    finally:
+        _lib.control(timeout_s=10.0)
+        _lib.control_reset()
