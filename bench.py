@@ -260,7 +260,9 @@ def run_gpu(args, cfg):
         return out
 
     clocks = ClockSampler(local).start() if rank == 0 else None
-    for _ in range(max(args.warmup, 3)):
+    from paper_2407_04656_b200.layer import run_step
+    run_step([layer], lambda: step(x, dout))   # grows the exchange buffers if the plan needs
+    for _ in range(max(args.warmup, 3) - 1):
         step(x, dout)
     torch.cuda.synchronize()
     layer.check()

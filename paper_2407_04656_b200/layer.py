@@ -592,6 +592,28 @@ class _MoEFunction(torch.autograd.Function):
         return (*grads, None)
 
 
+def run_step(layers, step_fn, max_reruns: int = 3):
+    """Run one training step ``step_fn()`` (forward + backward through ``layers``), check
+    every layer, and apply the exchange-capacity protocol: a plan that needs more exchange
+    rows raises the same ExchangeCapacityError on every rank (nothing was exchanged), so
+    every rank grows its buffers (``reserve``) and re-runs the step.  Returns step_fn's
+    value of the successful run.  StepAbortedError (a lost peer) propagates."""
+    from .dispatch import ExchangeCapacityError
+    for attempt in range(max_reruns + 1):
+        out = step_fn()
+        torch.cuda.synchronize()
+        try:
+            for L in layers:
+                L.check()
+            return out
+        except ExchangeCapacityError as exc:
+            if attempt == max_reruns:
+                raise
+            for L in layers:
+                L.reserve(exc.rows)
+    raise AssertionError("unreachable")
+
+
 def zipf_router_bias(n_experts: int, s: float, seed: int = 0) -> torch.Tensor:
     """log p_e with p_e ~ (1 + pi(e))^-s for a seeded permutation pi: makes the learned
     router's top-k a Zipf(s) sample (SURVEY.md 8d synthetic inputs)."""
@@ -607,4 +629,4 @@ def default_slots(n_experts: int, n_ranks: int, factor: int = 3) -> int:
     return math.ceil(factor * n_experts / n_ranks)
 
 
-__all__ = ["MoELayer", "StepAbortedError", "zipf_router_bias", "default_slots"]
+__all__ = ["MoELayer", "StepAbortedError", "run_step", "zipf_router_bias", "default_slots"]
