@@ -914,7 +914,9 @@ def run_elastic(args, cfg):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     E, k, d, dff, Tn = cfg["E"], cfg["k"], cfg["d"], cfg["dff"], cfg["tokens"]
-    c = math.ceil(cfg["slot_factor"] * E / world)
+    # slots per GPU held at the 8-GPU value whatever the starting N (slots are per-GPU
+    # memory)
+    c = math.ceil(cfg["slot_factor"] * E / 8)
     bias = zipf_router_bias(E, cfg["s"], seed=0)
     layer = MoELayer(d, dff, E, k, seed=0, router_bias=bias, device=dev,
                      router_std=1.28 / math.sqrt(d), group=dist.group.WORLD)
@@ -973,7 +975,8 @@ def run_elastic(args, cfg):
                 "steps": args.steps, "warmup": max(args.warmup, 3),
                 "ms_per_step": last["ms_per_step"], "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-                "config": {"workload": cfg["name"], "slots_per_gpu": c, "start_gpus": world},
+                "config": {"workload": cfg["name"], "slots_per_gpu": c, "start_gpus": world,
+                           "sequence": "->".join(str(p["n_gpus"]) for p in phases)},
                 "phases": phases, "reconfigurations": reconf}
         emit(line)
     dist.barrier(group=group)
