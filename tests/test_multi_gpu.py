@@ -23,7 +23,7 @@ def test_dist_layer(env):
     n = min(n, 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", "29533",
-           os.path.join(ROOT, "tests", "dist_layer_check.py"), "--rebalance"]
+           os.path.join(ROOT, "tests", "dist_layer_check.py"), "--rebalance", "--multilayer"]
     if n > 2 and not env:
         cmd.append("--elastic")
     if not env:
