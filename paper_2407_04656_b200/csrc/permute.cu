@@ -86,6 +86,104 @@ __global__ void __launch_bounds__(kRowThreads) pack_kernel(
   }
 }
 
+// Bulk-copy (TMA engine) variant of the pack: rows go HBM -> smem -> HBM through
+// cp.async.bulk, the SM only issues the copies.  Lane 0 of each warp drives a ring of
+// kPbSlots row slots: the loads of the next kPbSlots - 1 tokens of the warp are in flight
+// while the current token's row is stored to its k destinations (peers' buffers over
+// NVLink included) by bulk stores; a slot is refilled once its stores have read it
+// (bulk_group accounting).  Lanes < k write the return-map entries; pad rows are zeroed
+// with plain stores as in pack_kernel.  Selected with LZ_PACK_BULK=1 (A/B: DESIGN.md 4).
+constexpr int kPbWarps = 8, kPbSlots = 8;
+__device__ __forceinline__ uint32_t pb_smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__global__ void __launch_bounds__(32 * kPbWarps, 1) pack_bulk_kernel(
+    const uint4* __restrict__ x, int Tn, int d, int k, const int32_t* __restrict__ row,
+    const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers,
+    uint4* __restrict__ out, int E, const int32_t* __restrict__ recv_m,
+    const int32_t* __restrict__ recv_off, long n_pad_items,
+    const unsigned long long* __restrict__ ret_peers, long long* __restrict__ ret_own,
+    int my_rank, const int32_t* __restrict__ ret_row) {
+  extern __shared__ __align__(128) uint8_t pb_smem[];
+  __shared__ __align__(8) uint64_t pb_bar[kPbWarps][kPbSlots];
+  pdl_prologue();
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  const uint32_t rb = (uint32_t)d * 2;
+  uint8_t* ring = pb_smem + (size_t)warp * kPbSlots * rb;
+  const long gw = (long)blockIdx.x * kPbWarps + warp;
+  const long nw = (long)gridDim.x * kPbWarps;
+  const int nch = d / 8;
+  if (lane == 0) {
+    for (int j = 0; j < kPbSlots; ++j)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pb_smem_u32(&pb_bar[warp][j])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  auto load = [&](long i) {   // token gw + i * nw into slot i % kPbSlots (lane 0)
+    const long t = gw + i * nw;
+    const int j = (int)(i % kPbSlots);
+    const uint32_t bar = pb_smem_u32(&pb_bar[warp][j]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rb)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            pb_smem_u32(ring + (size_t)j * rb)),
+        "l"(x + t * nch), "r"(rb), "r"(bar)
+        : "memory");
+  };
+  const long ntok = gw < Tn ? (Tn - gw + nw - 1) / nw : 0;   // this warp's tokens
+  if (lane == 0)
+    for (long i = 0; i < kPbSlots && i < ntok; ++i) load(i);
+  uint32_t phases = 0;   // one parity bit per slot
+  for (long i = 0; i < ntok; ++i) {
+    const long t = gw + i * nw;
+    const int my_row = lane < k ? __ldg(row + t * k + lane) : 0;
+    const int my_rk = (peers && lane < k) ? __ldg(prank + t * k + lane) : 0;
+    if (ret_peers && lane < k)
+      reinterpret_cast<long long*>(ret_peers[my_rk])[my_row] =
+          ((long long)my_rank << 32) | (long long)__ldg(ret_row + t * k + lane);
+    long dst[LZ_MAX_TOPK];
+    for (int s2 = 0; s2 < k; ++s2) {
+      const long r = __shfl_sync(0xffffffffu, my_row, s2);
+      const int rk = __shfl_sync(0xffffffffu, my_rk, s2);
+      dst[s2] = (long)((peers ? reinterpret_cast<uint4*>(peers[rk]) : out) + r * nch);
+    }
+    if (lane == 0) {
+      const int j = (int)(i % kPbSlots);
+      const uint32_t bar = pb_smem_u32(&pb_bar[warp][j]);
+      const uint32_t par = (phases >> j) & 1u;
+      uint32_t done = 0;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(par)
+            : "memory");
+      } while (!done);
+      phases ^= 1u << j;
+      const uint32_t src = pb_smem_u32(ring + (size_t)j * rb);
+      for (int s2 = 0; s2 < k; ++s2)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst[s2]),
+                     "r"(src), "r"(rb)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      // refill the previous token's slot: its stores (the second most recent group) have
+      // finished reading it once at most one group is still reading
+      if (i >= 1 && i - 1 + kPbSlots < ntok) {
+        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        load(i - 1 + kPbSlots);
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  __syncwarp();
+  // pad rows of the expert-major layout (and their return-map entries)
+  for (long q = gw; q < n_pad_items; q += nw)
+    zero_pad_rows(out, d, E, recv_m, recv_off, q, n_pad_items, lane, ret_own);
+}
+
 __global__ void __launch_bounds__(kRowThreads) combine_kernel(
     const uint4* __restrict__ y, const int32_t* __restrict__ row, const int32_t* __restrict__ prank,
     const unsigned long long* __restrict__ peers, const float* __restrict__ w, int Tn, int d, int k,
@@ -708,6 +806,23 @@ static lz_status pack_impl(const void* x, int Tn, int d, int k, const int32_t* r
   if (E > 0 && (!recv_m || !recv_off || !out)) return LZ_ERR_ARG;
   const long npad = E > 0 ? pad_items(E, recv_m, recv_off, kPadAlign) : 0;
   if (Tn + npad == 0) return LZ_OK;
+  static const bool bulk = [] {
+    const char* e = getenv("LZ_PACK_BULK");
+    return e && atoi(e) != 0;
+  }();
+  const size_t pb_smem = (size_t)kPbWarps * kPbSlots * d * 2;
+  if (bulk && pb_smem <= 200 * 1024 && d % 8 == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(pack_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+    return lzh::launch(pack_bulk_kernel, dim3(lzh::num_sms()), dim3(32 * kPbWarps), pb_smem,
+                       (cudaStream_t)stream, 1, (const uint4*)x, Tn, d, k, row, prank, peers,
+                       (uint4*)out, E, recv_m, recv_off, npad, ret_peers, ret_own, my_rank,
+                       ret_row);
+  }
   return lzh::launch(pack_kernel, dim3(row_grid(Tn + npad)), dim3(kRowThreads), 0,
                      (cudaStream_t)stream, 1, (const uint4*)x, Tn, d, k, row, prank, peers,
                      (uint4*)out, E, recv_m, recv_off, npad, ret_peers, ret_own, my_rank, ret_row);
