@@ -317,13 +317,17 @@ __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uin
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-template <int KS>
+// ET > 0: the expert count is a compile-time constant (the common E = 8, 16, 32, 64), so
+// every router-weight and probability address offset folds into the instruction
+// (ncu r02: a third of the kernel's instructions were integer address arithmetic)
+template <int KS, int ET>
 __global__ void __launch_bounds__(32 * kDWarps) dispatch_bwd_kernel(
     const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
     int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
-    const float* __restrict__ dwv, const __nv_bfloat16* __restrict__ wg, int E, int renorm,
+    const float* __restrict__ dwv, const __nv_bfloat16* __restrict__ wg, int E_rt, int renorm,
     uint4* __restrict__ dx, float* __restrict__ dlogits) {
+  const int E = ET > 0 ? ET : E_rt;
   __shared__ __align__(16) float s_dl[kDWarps][64][kDT + 1];    // [expert][token]
   __shared__ __align__(16) float s_rt[kDWarps][kDT][64 + 4];    // router term, one pass
   __shared__ long long s_src[kDWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
@@ -940,15 +944,22 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
   long dgrid = (dtasks + kDWarps - 1) / kDWarps;
   const long dcap = (long)lzh::num_sms() * 16;
   if (dgrid > dcap) dgrid = dcap;
-#define LZ_DBWD(ks)                                                                          \
-  lzh::launch(dispatch_bwd_kernel<ks>, dim3((int)dgrid), dim3(32 * kDWarps), 0,                 \
+#define LZ_DBWD(ks, et)                                                                      \
+  lzh::launch(dispatch_bwd_kernel<ks, et>, dim3((int)dgrid), dim3(32 * kDWarps), 0,             \
               (cudaStream_t)stream, 1, (const uint4*)dxe, row, prank, peers, Tn, d, k, probs,   \
               idx, dw, (const __nv_bfloat16*)wg, E, renorm, (uint4*)dx, dlogits)
-  switch ((E + 15) / 16) {
-    case 1: LZ_DBWD(1); break;
-    case 2: LZ_DBWD(2); break;
-    case 3: LZ_DBWD(3); break;
-    default: LZ_DBWD(4); break;
+  switch (E) {
+    case 8: LZ_DBWD(1, 8); break;
+    case 16: LZ_DBWD(1, 16); break;
+    case 32: LZ_DBWD(2, 32); break;
+    case 64: LZ_DBWD(4, 64); break;
+    default:
+      switch ((E + 15) / 16) {
+        case 1: LZ_DBWD(1, 0); break;
+        case 2: LZ_DBWD(2, 0); break;
+        case 3: LZ_DBWD(3, 0); break;
+        default: LZ_DBWD(4, 0); break;
+      }
   }
 #undef LZ_DBWD
   return lzh::check_launch();
