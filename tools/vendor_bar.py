@@ -28,7 +28,14 @@ from paper_2407_04656_b200 import _lib, ops  # noqa: E402
 from paper_2407_04656_b200.layer import zipf_router_bias  # noqa: E402
 
 
+COOL_S = float(os.environ.get("VB_COOL_S", "0"))
+
+
 def timeit(fn, reps=20, warm=3):
+    if COOL_S > 0:   # let the board recover from the previous kernel's power draw
+        torch.cuda.synchronize()
+        import time
+        time.sleep(COOL_S)
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
@@ -41,12 +48,29 @@ def timeit(fn, reps=20, warm=3):
     return a.elapsed_time(b) / reps
 
 
+def best(results):
+    """Merge repeated runs of the same shape: the best (max TFLOP/s) of each kernel, so the
+    board's power-state drift over the run does not favour whichever kernel ran first."""
+    out = dict(results[0])
+    for key, val in results[0].items():
+        if isinstance(val, dict) and key != "errors":
+            for impl in val:
+                cands = [r[key][impl] for r in results if key in r and impl in r[key]]
+                out[key][impl] = max(cands, key=lambda c: c["TFLOPs"])
+                out[key][impl]["runs"] = [c["TFLOPs"] for c in cands]
+    return out
+
+
 def group_sizes(E, k, T, s, seed=0):
     g = torch.Generator().manual_seed(seed)
     bias = zipf_router_bias(E, s, seed=0)
     logits = bias + (-torch.log(-torch.log(torch.rand(T, E, generator=g))))
     idx = logits.topk(k, dim=1).indices
     return torch.bincount(idx.view(-1), minlength=E).tolist()
+
+
+def off_u(m, e):
+    return sum(m[:e])
 
 
 def run_shape(name, E, k, T, d, dff, s, out):
@@ -105,8 +129,14 @@ def run_shape(name, E, k, T, d, dff, s, out):
     m8 = [(v + 7) // 8 * 8 for v in m]
     P8 = sum(m8)
     offs8 = torch.tensor(list(torch.tensor(m8).cumsum(0)), dtype=torch.int32, device=dev)
+    # random data (zeros would let the tensor cores idle at a lower power draw)
     dYt8 = torch.zeros(d, P8, dtype=torch.bfloat16, device=dev)
     A8 = torch.zeros(P8, dff, dtype=torch.bfloat16, device=dev)
+    o8 = 0
+    for e in range(E):
+        dYt8[:, o8:o8 + m[e]] = dYu[off_u(m, e):off_u(m, e) + m[e]].t()
+        A8[o8:o8 + m[e]] = Au[off_u(m, e):off_u(m, e) + m[e]]
+        o8 += m8[e]
     try:
         rec("wgrad2", "torch._grouped_mm",
             timeit(lambda: torch._grouped_mm(dYt8, A8, offs=offs8)), f1)
@@ -173,8 +203,11 @@ def main():
     args = ap.parse_args()
     _lib.load()
     out = []
-    run_shape("cfg2", 16, 2, 65536, 1024, 4096, 1.2, out)
-    run_shape("cfg3", 8, 2, 16384, 4096, 14336, 1.2, out)
+    for shape in (("cfg2", 16, 2, 65536, 1024, 4096, 1.2), ("cfg3", 8, 2, 16384, 4096, 14336, 1.2)):
+        runs = []
+        for _ in range(3):
+            run_shape(*shape, runs)
+        out.append(best(runs))
     if args.fused:
         run_fused_moe(out)
     if args.json:
