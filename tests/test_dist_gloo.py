@@ -194,3 +194,109 @@ def test_expert_state_migration_moves_optimizer_state():
     dst = res[1][0][0]     # rank 1's expert 0 after the move
     assert len(src) == 6 and src == dst
     assert res[1][3] == 1
+
+
+def _fabric_worker(rank, n, port, q):
+    """comm.ProcessFabric serving the layer's exchange requests over gloo (CPU tensors):
+    HIST (all-gather), A2A (row all-to-all-v), ALLREDUCE, EXPERT_AR (replica groups), WAIT,
+    SYNC -- the same request stream the MoE layer's per-rank step yields."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=n)
+    try:
+        fab = comm.ProcessFabric(None)
+        assert (fab.rank, fab.world) == (rank, n)
+        hist = torch.tensor([rank, 10 + rank, 20 + rank], dtype=torch.int32)
+        T = fab.serve((comm.HIST, hist))
+        assert T.tolist() == [[j + 10 * e for j in range(n)] for e in range(3)]   # T[e][j]
+        # A2A: rank i sends (j + 1) rows to rank j, row value 100 i + j
+        send_sizes = [j + 1 for j in range(n)]
+        recv_counts = [rank + 1] * n
+        inp = torch.cat([torch.full((j + 1, 4), float(100 * rank + j)) for j in range(n)])
+        out = torch.empty(sum(recv_counts), 4)
+        fab.serve((comm.A2A, out, inp, recv_counts, send_sizes))
+        want = torch.cat([torch.full((rank + 1, 4), float(100 * i + rank)) for i in range(n)])
+        assert torch.equal(out, want)
+        flat = torch.full((5,), float(rank + 1))
+        fab.serve((comm.ALLREDUCE, flat))
+        assert torch.equal(flat, torch.full((5,), float(sum(range(1, n + 1)))))
+
+        class L:   # the two attributes EXPERT_AR reads from the layer
+            pass
+        R = [[1] * n, [1 if j == 0 else 0 for j in range(n)], [1] * n]
+        lay = L()
+        lay.local_ids = [e for e in range(3) if R[e][rank] > 0]
+        lay.replica_groups = fab.replica_groups(R)
+        g = torch.stack([torch.full((2, 2), float(rank + 1)) for _ in lay.local_ids])
+        works = fab.serve((comm.EXPERT_AR, lay, [g]))
+        fab.serve((comm.WAIT, works))
+        for p, e in enumerate(lay.local_ids):
+            owners = [j for j in range(n) if R[e][j] > 0]
+            assert torch.equal(g[p], torch.full((2, 2), float(sum(j + 1 for j in owners))))
+        assert fab.serve((comm.SYNC,)) is None
+        q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_process_fabric_serves_layer_requests(n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_fabric_worker, args=(r, n, port, q)) for r in range(n)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(n)]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, msg in res:
+        assert msg == "ok", f"rank {rank}:\n{msg}"
+
+
+def test_loopback_world_serves_requests_on_cpu_tensors():
+    """LoopbackWorld's request serving (HIST stack, A2A copies, ALLREDUCE, EXPERT_AR owner-
+    set sums, lockstep divergence detection, lost-rank collectives) on CPU tensors."""
+    from paper_2407_04656_b200 import loopback as LB
+    world = LB.LoopbackWorld.__new__(LB.LoopbackWorld)   # no CUDA streams needed here
+    world.n, world.lost, world.requests, world._alloc = 3, set(), 0, None
+    hs = {r: torch.tensor([r, r + 5], dtype=torch.int32) for r in range(3)}
+    T = world.serve(comm.HIST, {r: (comm.HIST, hs[r]) for r in range(3)})[0]
+    assert T.tolist() == [[0, 1, 2], [5, 6, 7]]
+    outs = {r: torch.empty(3 * (r + 1), 2) for r in range(3)}
+    inps = {r: torch.cat([torch.full((j + 1, 2), float(10 * r + j)) for j in range(3)])
+            for r in range(3)}
+    world.serve(comm.A2A, {r: (comm.A2A, outs[r], inps[r], [r + 1] * 3, [1, 2, 3])
+                           for r in range(3)})
+    for r in range(3):
+        want = torch.cat([torch.full((r + 1, 2), float(10 * i + r)) for i in range(3)])
+        assert torch.equal(outs[r], want)
+    flats = {r: torch.full((3,), float(r)) for r in range(3)}
+    world.serve(comm.ALLREDUCE, {r: (comm.ALLREDUCE, flats[r]) for r in range(3)})
+    assert all(torch.equal(f, torch.full((3,), 3.0)) for f in flats.values())
+
+    class L:
+        E = 2
+    layers = {}
+    for r in range(3):
+        layers[r] = L()
+        layers[r].local_ids = [0, 1] if r < 2 else [1]
+    grads = {r: torch.stack([torch.full((2,), float(r + 1))] * len(layers[r].local_ids))
+             for r in range(3)}
+    world.serve(comm.EXPERT_AR, {r: (comm.EXPERT_AR, layers[r], [grads[r]]) for r in range(3)})
+    assert grads[0][0].tolist() == [3.0, 3.0] and grads[1][0].tolist() == [3.0, 3.0]   # e0: 0,1
+    assert grads[0][1].tolist() == [6.0, 6.0] and grads[2][0].tolist() == [6.0, 6.0]   # e1: all
+
+    def gen(kinds):
+        for kd in kinds:
+            yield (kd,)
+        return "done"
+    assert world.run([gen([comm.SYNC, comm.SYNC]) for _ in range(3)]) == ["done"] * 3
+    with pytest.raises(RuntimeError, match="diverged"):
+        world.run([gen([comm.SYNC]), gen([comm.WAIT]), gen([comm.SYNC])])
+    world.lost = {2}
+    with pytest.raises(LB.PeerLostError):
+        world.serve(comm.HIST, {r: (comm.HIST, hs[r]) for r in range(2)})
