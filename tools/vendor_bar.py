@@ -162,30 +162,40 @@ def run_shape(name, E, k, T, d, dff, s, out):
     print(json.dumps(res), flush=True)
 
 
-def run_fused_moe(out):
-    """Whole-layer forward (routing given) of the Mixtral shape: lz (pack + 2 grouped GEMMs
-    with the SwiGLU epilogue + combine) vs flashinfer's fused MoE kernels."""
+def run_fused_moe(out, shape="cfg3"):
+    """Whole-layer forward (routing given to flashinfer; lz's forward also runs its own gate
+    and plan) of the cfg3 Mixtral shape (SwiGLU) or the cfg2 GPT shape (GELU MLP): lz (gate +
+    plan + pack + 2 grouped GEMMs with fused epilogues + combine) vs flashinfer's
+    cutlass_fused_moe (TensorRT-LLM CUTLASS MoE, prebuilt sm100 module)."""
+    from flashinfer.fused_moe import ActivationType
+
     from paper_2407_04656_b200.layer import MoELayer
     dev = torch.device("cuda")
-    E, k, T, d, dff = 8, 2, 16384, 4096, 14336
-    res = {"shape": "cfg3 forward (routing given)", "E": E, "k": k, "tokens": T, "d": d,
-           "d_ff": dff}
-    layer = MoELayer(d, dff, E, k, seed=0, activation="swiglu", device=dev,
+    if shape == "cfg3":
+        E, k, T, d, dff, act = 8, 2, 16384, 4096, 14336, "swiglu"
+    else:
+        E, k, T, d, dff, act = 16, 2, 65536, 1024, 4096, "gelu"
+    res = {"shape": f"{shape} forward (routing given)", "E": E, "k": k, "tokens": T, "d": d,
+           "d_ff": dff, "activation": act}
+    layer = MoELayer(d, dff, E, k, seed=0, activation=act, device=dev,
                      router_bias=zipf_router_bias(E, 1.2), router_std=1.28 / math.sqrt(d))
     x = torch.randn(T, d, device=dev).bfloat16()
-    flops = 2.0 * T * k * d * dff * 3
+    flops = 2.0 * T * k * d * dff * (3 if act == "swiglu" else 2)
     with torch.no_grad():
         res["lz_layer_fwd"] = {"ms": round(timeit(lambda: layer(x)), 4)}
     res["lz_layer_fwd"]["TFLOPs"] = round(flops / res["lz_layer_fwd"]["ms"] / 1e9, 1)
     idx, w, _, _ = ops.router_gate(x, layer.wg.detach(), layer.bg.detach(), k)
     try:
         from flashinfer.fused_moe import cutlass_fused_moe
-        # flashinfer's layout: fc1 [E, 2 d_ff, d] (W3 | W1 for Swiglu), fc2 [E, d, d_ff]
-        fc1 = (torch.randn(E, 2 * dff, d, device=dev) * 0.02).bfloat16()
+        # flashinfer's layout: fc1 [E, 2 d_ff, d] (W3 | W1, Swiglu) or [E, d_ff, d] (Gelu),
+        # fc2 [E, d, d_ff]
+        f1 = 2 * dff if act == "swiglu" else dff
+        fc1 = (torch.randn(E, f1, d, device=dev) * 0.02).bfloat16()
         fc2 = (torch.randn(E, d, dff, device=dev) * 0.02).bfloat16()
         outb = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        at = ActivationType.Swiglu if act == "swiglu" else ActivationType.Gelu
         fn = lambda: cutlass_fused_moe(x, idx, w, fc1, fc2, torch.bfloat16, [],  # noqa: E731
-                                       output=outb)
+                                       output=outb, tune_max_num_tokens=T, activation_type=at)
         ms = timeit(fn)
         res["flashinfer.cutlass_fused_moe"] = {"ms": round(ms, 4),
                                                "TFLOPs": round(flops / ms / 1e9, 1)}
@@ -209,7 +219,8 @@ def main():
             run_shape(*shape, runs)
         out.append(best(runs))
     if args.fused:
-        run_fused_moe(out)
+        for shape in ("cfg2", "cfg3"):
+            run_fused_moe(out, shape)
     if args.json:
         with open(args.json, "w") as f:
             json.dump({"gpu": torch.cuda.get_device_name(), "results": out}, f, indent=1)
