@@ -34,6 +34,7 @@ constexpr int kMaxGroups = 128;
 constexpr int kEpiCols = 32;
 constexpr int kEpiBuf = 32 * kEpiCols * 2;          // 2 KB
 constexpr int kBarBytes = 256;
+constexpr int kSchedSlots = 4;   // dynamic scheduler queue depth
 constexpr int kTabBytes = 3 * (kMaxGroups + 1) * 4;  // s_off, s_pref, s_perm
 
 // CG = 1: one CTA per 128 x 256 tile (UMMA 128x256x16, cta_group::1), 3-4 stages x 48 KB.
@@ -398,6 +399,10 @@ struct Params {
   // W1|W3 is 235 MB per expert: n-fastest order re-read it from DRAM for every m-block,
   // 27 GB per launch)
   long long l2_chunk_bytes;
+  // dynamic tile scheduler (non-null): [0] next tile, [1] units done -- the leader CTA of
+  // each unit fetches tiles with an atomic add and hands them to its roles (and to the
+  // peer CTA) through a shared-memory queue; the last unit resets both counters
+  int* tile_ctr;
 };
 
 // Tile `local` of an (n_outer x n_inner) grid, ordered: for each chunk of `c` inner
@@ -743,7 +748,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty_bar = full_bar + C::kStages;
   uint64_t* tfull_bar = empty_bar + C::kStages;
   uint64_t* tempty_bar = tfull_bar + 2;
-  uint32_t* s_tmem = (uint32_t*)(tempty_bar + 2);
+  uint64_t* sched_full = tempty_bar + 2;             // [kSchedSlots] tile id published
+  uint64_t* sched_empty = sched_full + kSchedSlots;   // [kSchedSlots] all roles read it
+  int32_t* s_sched = (int32_t*)(sched_empty + kSchedSlots);   // [kSchedSlots] tile ids
+  uint32_t* s_tmem = (uint32_t*)(s_sched + kSchedSlots);
   int32_t* s_total0 = (int32_t*)(s_tmem + 1);   // class-0 tile count (mode 0)
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
@@ -809,6 +817,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull_bar[s], 1);
       mbar_init(&tempty_bar[s], kEpiWarps * CG);  // one arrival per epilogue warp of each CTA
     }
+    for (int s = 0; s < kSchedSlots; ++s) {
+      mbar_init(&sched_full[s], 1);
+      // read by: the MMA warp and every epilogue warp of the leader, the peer's producer and
+      // every epilogue warp of the peer
+      mbar_init(&sched_empty[s], CG == 1 ? 1 + kEpiWarps : 2 + 2 * kEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -835,6 +849,62 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem_base = *s_tmem;
   const int total0 = *s_total0;
   const int total = s_pref[p.G] + total0;
+  const bool dyn = p.tile_ctr != nullptr;
+  // Tile feed of one role.  Static: the snake schedule.  Dynamic: the leader CTA's producer
+  // fetches with an atomic add and publishes into the queue (also into the peer CTA's);
+  // every other role reads the queue and releases the slot to the leader's producer.
+  int f_w = 0, f_q = 0;
+  uint32_t f_ph = 0;
+  auto next_tile = [&](bool publisher) -> int {
+    if (!dyn) {
+      const int t = sched_tile(f_w, unit, nunits);
+      ++f_w;
+      return t;
+    }
+    int tile;
+    if (publisher) {
+      mbar_wait(&sched_empty[f_q], f_ph ^ 1);
+      tile = atomicAdd(p.tile_ctr, 1);
+      if (tile > total) tile = total;
+      s_sched[f_q] = tile;
+      if (CG == 2) {
+        asm volatile(
+            "{\n\t.reg .b32 ra, rb;\n\t"
+            "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
+            "st.shared::cluster.s32 [ra], %2;\n\t"
+            "mapa.shared::cluster.u32 rb, %1, 1;\n\t"
+            "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [rb];\n\t}" ::"r"(
+                smem_u32(&s_sched[f_q])),
+            "r"(smem_u32(&sched_full[f_q])), "r"(tile)
+            : "memory");
+      }
+      mbar_arrive(&sched_full[f_q]);
+    } else {
+      mbar_wait(&sched_full[f_q], f_ph);
+      tile = *reinterpret_cast<volatile int32_t*>(&s_sched[f_q]);
+      // the producer role runs on one lane, the MMA and epilogue roles on whole warps:
+      // one release per role instance, after all of its lanes have read the slot
+      const unsigned am = __activemask();
+      __syncwarp(am);
+      if (lane == __ffs(am) - 1) {
+        if (CG == 1 || leader) {
+          mbar_arrive(&sched_empty[f_q]);
+        } else {
+          asm volatile(
+              "{\n\t.reg .b32 ra;\n\t"
+              "mapa.shared::cluster.u32 ra, %0, 0;\n\t"
+              "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(
+                  smem_u32(&sched_empty[f_q]))
+              : "memory");
+        }
+      }
+    }
+    if (++f_q == kSchedSlots) {
+      f_q = 0;
+      f_ph ^= 1;
+    }
+    return tile;
+  };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -842,8 +912,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       bool arrived = p.flags == nullptr;
-      for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
-           tile = sched_tile(++w, unit, nunits)) {
+      for (int tile = next_tile(leader); tile < total; tile = next_tile(leader)) {
         const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
         if (t.remote && !arrived) {   // first tile with rows from other ranks
           wait_arrivals(p);
@@ -872,6 +941,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      if (dyn && leader) {
+        // this unit fetched its end marker: the last unit to get here resets the counters
+        // for the next launch (no unit fetches after its own end marker)
+        __threadfence();
+        if (atomicAdd(p.tile_ctr + 1, 1) == nunits - 1) {
+          p.tile_ctr[0] = 0;
+          p.tile_ctr[1] = 0;
+          __threadfence();
+        }
+      }
     }
   } else if (warp == 1) {
     if (leader) {
@@ -891,8 +970,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
-           tile = sched_tile(++w, unit, nunits)) {
+      for (int tile = next_tile(false); tile < total; tile = next_tile(false)) {
         const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
@@ -931,8 +1009,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kChunks = BN / kEpiCols / (kEpiWarps / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int w = 0, tile = sched_tile(0, unit, nunits); tile < total;
-           tile = sched_tile(++w, unit, nunits)) {
+    for (int tile = next_tile(false); tile < total; tile = next_tile(false)) {
       const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
@@ -1128,6 +1205,27 @@ static bool make_map(CUtensorMap* m, const void* base, uint64_t inner, uint64_t 
 }
 
 static int g_cta_group = 2;  // default: CTA-pair kernel
+
+// Dynamic tile scheduler counters (Params::tile_ctr): a rolling pool of counter pairs, one
+// per launch, each reset to zero by the last unit of its launch (so a slot is reusable,
+// also by every replay of a captured graph).  LZ_GEMM_DYNAMIC=0 keeps the static schedule.
+constexpr int kCtrSlots = 1024;
+__device__ int g_tile_ctr[kCtrSlots][2];
+static int* tile_counter() {
+  static const bool on = [] {
+    const char* e = getenv("LZ_GEMM_DYNAMIC");
+    return !e || atoi(e) != 0;
+  }();
+  if (!on) return nullptr;
+  static int* base = nullptr;
+  static unsigned next = 0;
+  if (!base) {
+    void* ptr = nullptr;
+    if (cudaGetSymbolAddress(&ptr, g_tile_ctr) != cudaSuccess) return nullptr;
+    base = (int*)ptr;
+  }
+  return base + 2 * (next++ % kCtrSlots);
+}
 // L2 budget of the re-read operand chunk (Params::l2_chunk_bytes); LZ_GEMM_L2_CHUNK_MB
 // overrides it for A/B runs (0 = no chunking: plain inner-fastest raster)
 static long long g_l2_chunk_bytes = [] {
@@ -1279,6 +1377,7 @@ static lz_status grouped_gemm_impl(int mode, const void* A, const void* B, void*
   p.n_flags = n_flags;
   p.epoch = epoch;
   p.l2_chunk_bytes = g_l2_chunk_bytes;
+  p.tile_ctr = tile_counter();
   cudaStream_t s = (cudaStream_t)stream;
   int sms = num_sms > 0 ? num_sms : lzh::num_sms();
   if (sms < 2) sms = 2;
