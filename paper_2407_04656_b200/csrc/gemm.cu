@@ -853,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Tile feed of one role.  Static: the snake schedule.  Dynamic: the leader CTA's producer
   // fetches with an atomic add and publishes into the queue (also into the peer CTA's);
   // every other role reads the queue and releases the slot to the leader's producer.
-  int f_w = 0, f_q = 0;
+  int f_w = 0, f_q = 0, f_pend = -1;
   uint32_t f_ph = 0;
   auto next_tile = [&](bool publisher) -> int {
     if (!dyn) {
@@ -863,9 +863,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int tile;
     if (publisher) {
+      // one fetch of lookahead: the atomic for the next tile is in flight while this
+      // tile's loads are issued (its latency was a bubble at every tile boundary)
+      if (f_pend < 0) f_pend = atomicAdd(p.tile_ctr, 1);
+      tile = f_pend < total ? f_pend : total;
+      if (tile < total) f_pend = atomicAdd(p.tile_ctr, 1);
       mbar_wait(&sched_empty[f_q], f_ph ^ 1);
-      tile = atomicAdd(p.tile_ctr, 1);
-      if (tile > total) tile = total;
       s_sched[f_q] = tile;
       if (CG == 2) {
         asm volatile(
