@@ -853,8 +853,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Tile feed of one role.  Static: the snake schedule.  Dynamic: the leader CTA's producer
   // fetches with an atomic add and publishes into the queue (also into the peer CTA's);
   // every other role reads the queue and releases the slot to the leader's producer.
-  int f_w = 0, f_q = 0, f_pend = -1;
+  int f_w = 0, f_q = 0, f_pend = -1, f_ahead = -1;
   uint32_t f_ph = 0;
+  // (publisher) publish tile t into queue slot f_q of both CTAs of the unit
+  auto publish = [&](int t) {
+    mbar_wait(&sched_empty[f_q], f_ph ^ 1);
+    s_sched[f_q] = t;
+    if (CG == 2) {
+      asm volatile(
+          "{\n\t.reg .b32 ra, rb;\n\t"
+          "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
+          "st.shared::cluster.s32 [ra], %2;\n\t"
+          "mapa.shared::cluster.u32 rb, %1, 1;\n\t"
+          "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [rb];\n\t}" ::"r"(
+              smem_u32(&s_sched[f_q])),
+          "r"(smem_u32(&sched_full[f_q])), "r"(t)
+          : "memory");
+    }
+    mbar_arrive(&sched_full[f_q]);
+    if (++f_q == kSchedSlots) {
+      f_q = 0;
+      f_ph ^= 1;
+    }
+  };
+  // (publisher) the next fetched tile; the atomic for the one after is already in flight
+  auto fetch = [&]() -> int {
+    const int t = f_pend;
+    f_pend = atomicAdd(p.tile_ctr, 1);
+    return t < total ? t : total;
+  };
   auto next_tile = [&](bool publisher) -> int {
     if (!dyn) {
       const int t = sched_tile(f_w, unit, nunits);
@@ -863,25 +890,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     int tile;
     if (publisher) {
-      // one fetch of lookahead: the atomic for the next tile is in flight while this
-      // tile's loads are issued (its latency was a bubble at every tile boundary)
-      if (f_pend < 0) f_pend = atomicAdd(p.tile_ctr, 1);
-      tile = f_pend < total ? f_pend : total;
-      if (tile < total) f_pend = atomicAdd(p.tile_ctr, 1);
-      mbar_wait(&sched_empty[f_q], f_ph ^ 1);
-      s_sched[f_q] = tile;
-      if (CG == 2) {
-        asm volatile(
-            "{\n\t.reg .b32 ra, rb;\n\t"
-            "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
-            "st.shared::cluster.s32 [ra], %2;\n\t"
-            "mapa.shared::cluster.u32 rb, %1, 1;\n\t"
-            "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [rb];\n\t}" ::"r"(
-                smem_u32(&s_sched[f_q])),
-            "r"(smem_u32(&sched_full[f_q])), "r"(tile)
-            : "memory");
+      // the queue runs one tile ahead of the publisher's own loads, so the peer CTA and the
+      // MMA / epilogue roles already know tile i+1 when tile i starts
+      if (f_ahead < 0) {
+        f_pend = atomicAdd(p.tile_ctr, 1);
+        f_ahead = fetch();
+        publish(f_ahead);
       }
-      mbar_arrive(&sched_full[f_q]);
+      tile = f_ahead;
+      if (tile < total) {
+        f_ahead = fetch();
+        publish(f_ahead);
+      }
+      return tile;
     } else {
       mbar_wait(&sched_full[f_q], f_ph);
       tile = *reinterpret_cast<volatile int32_t*>(&s_sched[f_q]);
