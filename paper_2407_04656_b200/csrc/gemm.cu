@@ -1235,17 +1235,18 @@ static int g_cta_group = 2;  // default: CTA-pair kernel
 // also by every replay of a captured graph).  LZ_GEMM_DYNAMIC=0 keeps the static schedule.
 constexpr int kCtrSlots = 1024;
 __device__ int g_tile_ctr[kCtrSlots][2];
-// Policy (LZ_GEMM_DYNAMIC unset): dynamic for the weight-gradient GEMMs (variable-K tiles:
-// 13-20 % faster than the static LPT schedule) and for row GEMMs launched on a reduced
-// grid next to NCCL (clusters that start late no longer own a fixed share of the tiles);
-// static for the full-grid row GEMMs (the short-K ones measured 6-8 % slower dynamic).
-// LZ_GEMM_DYNAMIC=1: always dynamic, 0: never.
+// Policy: LZ_GEMM_DYNAMIC=1 always dynamic, 2 = dynamic for the weight-gradient GEMMs and
+// the reduced-grid row GEMMs next to NCCL only, unset / 0 = the static snake schedule.
+// Measured (profiles/r02_gemm_dynamic_ab.log): launched alone, the weight-gradient GEMMs are
+// 13-20 % faster dynamic and the short-K row GEMMs 6-8 % slower; inside the whole step
+// (N = 1 and N = 4, interleaved runs) neither policy beats the static schedule beyond
+// run-to-run noise, so the static one stays the default.
 static int* tile_counter(int mode, int num_sms) {
   static const int pol = [] {
     const char* e = getenv("LZ_GEMM_DYNAMIC");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 0;
   }();
-  const bool on = pol == 1 || (pol < 0 && (mode == 1 || num_sms > 0));
+  const bool on = pol == 1 || (pol == 2 && (mode == 1 || num_sms > 0));
   if (!on) return nullptr;
   static int* base = nullptr;
   static unsigned next = 0;
