@@ -191,7 +191,8 @@ def run_reference(args, cfg):
     value = tok / total
     same = "cpu_tokens" not in cfg and (world == 1 or bool(cfg.get("virtual")))
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+        "impl": "reference", "metric": METRIC if cfg["bwd"] else METRIC.replace("fwd+bwd", "fwd"),
+        "value": value, "unit": "tokens/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
