@@ -266,8 +266,14 @@ def lzh_num_sms() -> int:
     return torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
 
 
+_NVTX = os.environ.get("LZ_NVTX", "0") == "1"   # NVTX ranges / marks for nsys & ncu
+
+
 def _mark(layer, name: str, stream=None) -> None:
-    """Stage timing (bench --breakdown): CUDA event on ``stream`` (default: current)."""
+    """Stage timing (bench --breakdown): CUDA event on ``stream`` (default: current); with
+    LZ_NVTX=1 also an NVTX mark named after the stage that just ended."""
+    if _NVTX:
+        torch.cuda.nvtx.mark(f"lz.{name}")
     if layer.stage_events is not None:
         s = stream if stream is not None else torch.cuda.current_stream()
         e = torch.cuda.Event(enable_timing=True)
@@ -577,7 +583,11 @@ class _MoEFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, wg, bg, w1, w2, layer: MoELayer):
         st: dict = {}
+        if _NVTX:
+            torch.cuda.nvtx.range_push("lz.moe_forward")
         out = layer.fabric.run(_forward_steps(layer, x, wg, bg, w1, w2, st))
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
         ctx.layer = layer
         ctx.st = st
         ctx.save_for_backward(x, wg, w1, w2)
@@ -587,7 +597,11 @@ class _MoEFunction(torch.autograd.Function):
     def backward(ctx, dout):
         x, wg, w1, w2 = ctx.saved_tensors
         layer: MoELayer = ctx.layer
+        if _NVTX:
+            torch.cuda.nvtx.range_push("lz.moe_backward")
         grads = layer.fabric.run(_backward_steps(layer, ctx.st, x.contiguous(), wg, w1, w2, dout))
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
         ctx.st = None
         return (*grads, None)
 
