@@ -480,6 +480,7 @@ def run_gpu(args, cfg):
         ms_e2e = float(t.item())
 
     clk = clocks.stop() if clocks else None
+    layer.check()   # the timed steps' plans were valid and fit the exchange buffers
 
     if rank == 0:
         hbm, tf_burst, tf_sus, src = _peaks()
@@ -931,11 +932,21 @@ def run_elastic(args, cfg):
     layer.set_plan(replica_matrix(plan_for_loads(loads, world, c, 2)))
     group = dist.group.WORLD
 
+    from paper_2407_04656_b200.layer import run_step
+
+    def one_step():
+        layer.zero_grad(set_to_none=True)
+        layer(x).backward(dout)
+
     def measure(grp):
-        for _ in range(max(args.warmup, 3)):
-            layer.zero_grad(set_to_none=True)
-            layer(x).backward(dout)
+        # the first warm-up step applies the capacity protocol: a plan that needs more
+        # exchange rows (the survivors' plans are less balanced) grows the buffers before
+        # anything is timed; a step that overflowed exchanges nothing and must not be timed
+        run_step([layer], one_step)
+        for _ in range(max(args.warmup, 3) - 1):
+            one_step()
         torch.cuda.synchronize()
+        layer.check()
         dist.barrier(group=grp)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -944,6 +955,7 @@ def run_elastic(args, cfg):
             layer(x).backward(dout)
         e1.record()
         torch.cuda.synchronize()
+        layer.check()     # every timed step ran the full exchange
         t = torch.tensor([e0.elapsed_time(e1)], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=grp)
         n = dist.get_world_size(grp)
