@@ -8,6 +8,13 @@
 //   combine  PAPER.md:99 weighted sum of the k expert outputs (fixed s order)
 #include "common.cuh"
 
+#ifndef LZ_D2_STAGES
+#define LZ_D2_STAGES 2
+#endif
+#ifndef LZ_D2_BLOCKS
+#define LZ_D2_BLOCKS 4
+#endif
+
 namespace lz {
 
 constexpr int kRowThreads = 256;
@@ -297,14 +304,11 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
   }
 }
 
-// Gate backward (softmax + top-k (+renorm)) and dispatch backward.  A warp owns 16
-// tokens.  Phase A computes their dlogits (lane = expert) into smem.  Phase B sweeps the
-// row 64 columns at a time: the router term dlogits[16 x E] . wg[E x 64] runs on the
-// tensor cores (mma.sync m16n8k16, dlogits split into bf16 hi + lo so the product keeps
-// ~16 mantissa bits), is staged through smem, and joins the gathered expert rows
-// sum_s dxe[row(t, s)] in a 128-byte coalesced row pass.
+// Gate backward (softmax + top-k (+renorm)) and dispatch backward, fused per 16-token
+// tile: dlogits from probs / idx / dw, then dx = sum_s dxe[row(t, s)] + dlogits . wg with
+// the router term on the tensor cores (mma.sync m16n8k16, dlogits split into bf16 hi + lo
+// so the product keeps ~16 mantissa bits).
 constexpr int kDT = 16;
-constexpr int kDWarps = 4;
 __device__ __forceinline__ uint32_t bf16pair(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -317,174 +321,315 @@ __device__ __forceinline__ void mma16816(float* c, uint32_t a0, uint32_t a1, uin
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
-// ET > 0: the expert count is a compile-time constant (the common E = 8, 16, 32, 64), so
-// every router-weight and probability address offset folds into the instruction
-// (ncu r02: a third of the kernel's instructions were integer address arithmetic)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
+               "r"(pred ? 16 : 0)
+               : "memory");
+}
+// Register-direct variant.  The router-term MMA's output columns are permuted so that
+// each lane's C fragment covers 8 CONTIGUOUS row columns: in the 32-column block b, lane
+// (g, t4) of n8 tile nt holds columns b*32 + t4*8 + 2*nt + {0, 1} for tokens g and g + 8
+// (the B fragment of n8 tile nt therefore loads the router-weight columns
+// b*32 + (n >> 1)*8 + 2*nt + (n & 1), n = 0..7).  The lane then adds its tokens' gathered
+// expert rows (one 16-byte load per (token, s, block)) and stores dx -- no shared-memory
+// round trip of the router term, no column-pass barriers.  Phase A (dlogits) runs on all
+// 32 lanes: lane pair (2 ti, 2 ti + 1) owns token ti, each lane half of its experts.
+constexpr int kD2Warps = 4;
+constexpr int kD2Stages = LZ_D2_STAGES;
+constexpr int kD2Smem = kD2Warps * kD2Stages * 8 * 32 * 16;
+__device__ __forceinline__ uint4 ld_shared_u4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+// Phase-A inputs of one task (lane pair 2 ti, 2 ti + 1 = token ti; lane half h holds the
+// probabilities of experts [h EH, (h + 1) EH)); loaded one task ahead
+template <int EH>
+struct DbwdIn {
+  int id[2], row[2], rk[2];
+  float dw[2], pr[EH];
+};
+template <int EH>
+__device__ __forceinline__ void dbwd_load(DbwdIn<EH>& in, long t, int Tn, int k, int E, int h,
+                                          const int32_t* __restrict__ idx,
+                                          const float* __restrict__ dwv,
+                                          const int32_t* __restrict__ row,
+                                          const int32_t* __restrict__ prank,
+                                          const float* __restrict__ probs, bool peers) {
+  const bool ok = t < Tn;
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2) {
+    const bool o = ok && s2 < k;
+    in.id[s2] = o ? __ldg(idx + t * k + s2) : -1;
+    in.dw[s2] = o ? __ldg(dwv + t * k + s2) : 0.f;
+    in.row[s2] = o ? __ldg(row + t * k + s2) : 0;
+    in.rk[s2] = (o && peers) ? __ldg(prank + t * k + s2) : 0;
+  }
+#pragma unroll
+  for (int j = 0; j < EH; ++j) {
+    const int e = h * EH + j;
+    in.pr[j] = (ok && e < E) ? __ldg(probs + t * E + e) : 0.f;
+  }
+}
 template <int KS, int ET>
-__global__ void __launch_bounds__(32 * kDWarps) dispatch_bwd_kernel(
+__global__ void __launch_bounds__(32 * kD2Warps) dispatch_bwd_reg(
     const uint4* __restrict__ dxe, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers, int Tn, int d,
     int k, const float* __restrict__ probs, const int32_t* __restrict__ idx,
     const float* __restrict__ dwv, const __nv_bfloat16* __restrict__ wg, int E_rt, int renorm,
-    uint4* __restrict__ dx, float* __restrict__ dlogits) {
+    uint4* __restrict__ dx, float* __restrict__ dlogits, int nh) {
   const int E = ET > 0 ? ET : E_rt;
-  __shared__ __align__(16) float s_dl[kDWarps][64][kDT + 1];    // [expert][token]
-  __shared__ __align__(16) float s_rt[kDWarps][kDT][64 + 4];    // router term, one pass
-  __shared__ long long s_src[kDWarps][kDT][LZ_MAX_TOPK];        // row base per (token, s)
+  constexpr int EP = KS * 16;                 // experts padded to the MMA k steps
+  constexpr int EH = EP / 2;                  // experts per phase-A lane
+  __shared__ __align__(16) float s_dl[kD2Warps][kDT][EP + 4];
+  __shared__ long long s_src[kD2Warps][kDT][LZ_MAX_TOPK];
+  extern __shared__ __align__(16) uint4 d2_ring[];   // [warps][stages][8 slots][32 lanes]
   pdl_prologue();
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
-  const long gw = (long)blockIdx.x * kDWarps + warp;
-  const long nw = (long)gridDim.x * kDWarps;
+  const long gw = (long)blockIdx.x * kD2Warps + warp;
+  const long nw = (long)gridDim.x * kD2Warps;
   const int nch = d / 8;
-  const int g = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
-  const int tq = lane >> 3;                 // row pass: tokens 4*tq .. 4*tq+3
-  const int cq = lane & 7;                  // row pass: 16-byte chunk inside the 64 columns
-  for (long t0 = gw * kDT; t0 < Tn; t0 += nw * kDT) {
-    // ---- phase A: dlogits, one lane per token (lanes 0..15) ----------------------
-    // dp_e is non-zero only at the k routed experts, so
-    //   dot = sum_s g_s p_{idx_s},  dl_e = p_e (dp_e - dot)
-    // with g_s = dw_s (renorm: (dw_s - sum_s' dw_s' w_s') / S, S = sum_s p_{idx_s}).
-    if (lane < kDT) {
-      const int ti = lane;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int ti = lane >> 1, h = lane & 1;     // phase-A token / expert half
+  const uint32_t* wT = reinterpret_cast<const uint32_t*>(wg);
+  const long ntask = (long)((Tn + kDT - 1) / kDT) * nh;
+  const int dcols = d / nh;                   // columns of one task
+  const uint32_t ring = (uint32_t)__cvta_generic_to_shared(d2_ring) +
+                        (uint32_t)(warp * kD2Stages * 8 * 32 * 16) + lane * 16;
+  DbwdIn<EH> nxt;
+  if (gw < ntask)
+    dbwd_load<EH>(nxt, (gw / nh) * kDT + ti, Tn, k, E, h, idx, dwv, row, prank, probs,
+                  peers != nullptr);
+  for (long task = gw; task < ntask; task += nw) {
+    const long t0 = (task / nh) * kDT;
+    const int half = (int)(task % nh);
+    const DbwdIn<EH> in = nxt;
+    if (task + nw < ntask)   // next task's phase-A inputs in flight during this task
+      dbwd_load<EH>(nxt, ((task + nw) / nh) * kDT + ti, Tn, k, E, h, idx, dwv, row, prank,
+                    probs, peers != nullptr);
+    // ---- phase A: dlogits (dp_e is non-zero only at the k routed experts:
+    //   dot = sum_s g_s p_{idx_s},  dl_e = p_e (dp_e - dot), g_s = dw_s or its renorm form)
+    {
       const long t = t0 + ti;
+      float dl[EH];
+      // p_{idx_s} from the lane of the pair that holds expert idx_s (all lanes shuffle)
+      float pin[2];
+#pragma unroll
+      for (int s2 = 0; s2 < 2; ++s2) {
+        float mine = 0.f;
+#pragma unroll
+        for (int j = 0; j < EH; ++j)
+          if (in.id[s2] == h * EH + j) mine = in.pr[j];
+        const float other = __shfl_xor_sync(0xffffffffu, mine, 1);
+        pin[s2] = (in.id[s2] >= 0 && in.id[s2] / EH == h) ? mine : other;
+      }
       if (t < Tn) {
         int ids[LZ_MAX_TOPK];
         float gs[LZ_MAX_TOPK], ps[LZ_MAX_TOPK];
-        float S = 0.f, sdw = 0.f;
-        for (int s2 = 0; s2 < k; ++s2) {
-          const int e = __ldg(idx + t * k + s2);
+        float S = 0.f;
+#pragma unroll
+        for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2) {
+          ids[s2] = -1;
+          gs[s2] = ps[s2] = 0.f;
+          if (s2 >= k) continue;
+          int e, rr, rk;
+          float p;
+          if (s2 < 2) {
+            e = in.id[s2];
+            gs[s2] = in.dw[s2];
+            rr = in.row[s2];
+            rk = in.rk[s2];
+            p = pin[s2];
+          } else {
+            e = __ldg(idx + t * k + s2);
+            gs[s2] = __ldg(dwv + t * k + s2);
+            rr = __ldg(row + t * k + s2);
+            rk = peers ? __ldg(prank + t * k + s2) : 0;
+            p = __ldg(probs + t * E + e);
+          }
           ids[s2] = e;
-          gs[s2] = __ldg(dwv + t * k + s2);
-          ps[s2] = __ldg(probs + t * E + e);
-          S += ps[s2];
-          const int rr = __ldg(row + t * k + s2);
-          const int rk = peers ? __ldg(prank + t * k + s2) : 0;
-          const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[rk]) : dxe;
-          s_src[warp][ti][s2] = (long long)(base + (long)rr * nch);
+          ps[s2] = p;
+          S += p;
+          if (h == 0) {
+            const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[rk]) : dxe;
+            s_src[warp][ti][s2] = (long long)(base + (long)rr * nch);
+          }
         }
         if (renorm) {
-          for (int s2 = 0; s2 < k; ++s2) sdw += gs[s2] * (ps[s2] / S);
-          for (int s2 = 0; s2 < k; ++s2) gs[s2] = (gs[s2] - sdw) / S;
+          float sdw = 0.f;
+#pragma unroll
+          for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
+            if (s2 < k) sdw += gs[s2] * (ps[s2] / S);
+#pragma unroll
+          for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
+            if (s2 < k) gs[s2] = (gs[s2] - sdw) / S;
         }
         float dot = 0.f;
-        for (int s2 = 0; s2 < k; ++s2) dot += gs[s2] * ps[s2];
-        for (int e = 0; e < 64; ++e) s_dl[warp][e][ti] = 0.f;
-        for (int e = 0; e < E; ++e) s_dl[warp][e][ti] = -__ldg(probs + t * E + e) * dot;
-        for (int s2 = 0; s2 < k; ++s2) s_dl[warp][ids[s2]][ti] += ps[s2] * gs[s2];
-        for (int e = 0; e < E; ++e) dlogits[t * E + e] = s_dl[warp][e][ti];
+#pragma unroll
+        for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
+          if (s2 < k) dot += gs[s2] * ps[s2];
+#pragma unroll
+        for (int j = 0; j < EH; ++j) dl[j] = -in.pr[j] * dot;
+#pragma unroll
+        for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2) {
+#pragma unroll
+          for (int j = 0; j < EH; ++j)
+            if (ids[s2] == h * EH + j) dl[j] += ps[s2] * gs[s2];
+        }
+        if (half == 0) {
+          if (ET > 0 && ET % 8 == 0 && EH % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < EH; j += 4)
+              if (h * EH + j < E)
+                *reinterpret_cast<float4*>(dlogits + t * E + h * EH + j) =
+                    make_float4(dl[j], dl[j + 1], dl[j + 2], dl[j + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < EH; ++j)
+              if (h * EH + j < E) dlogits[t * E + h * EH + j] = dl[j];
+          }
+        }
       } else {
-        for (int e = 0; e < 64; ++e) s_dl[warp][e][ti] = 0.f;
+#pragma unroll
+        for (int j = 0; j < EH; ++j) dl[j] = 0.f;
       }
+#pragma unroll
+      for (int j = 0; j < EH; j += 4)
+        *reinterpret_cast<float4*>(&s_dl[warp][ti][h * EH + j]) =
+            make_float4(dl[j], dl[j + 1], dl[j + 2], dl[j + 3]);
     }
     __syncwarp();
     const int nt = (int)min((long)kDT, Tn - t0);
-    // A fragments (dlogits as hi + lo bf16), per 16-expert k step (E <= 64)
+    const bool v0 = g < nt, v1 = g + 8 < nt;
+    // A fragments: dlogits rows (tokens) x experts, bf16 hi + lo
     uint32_t ah[KS][4], al[KS][4];
 #pragma unroll
     for (int ks = 0; ks < KS; ++ks) {
-      {
-        const int e0 = ks * 16 + 2 * t4;
-        const float v[8] = {s_dl[warp][e0][g],     s_dl[warp][e0 + 1][g],
-                            s_dl[warp][e0][g + 8], s_dl[warp][e0 + 1][g + 8],
-                            s_dl[warp][e0 + 8][g], s_dl[warp][e0 + 9][g],
-                            s_dl[warp][e0 + 8][g + 8], s_dl[warp][e0 + 9][g + 8]};
+      const int e0 = ks * 16 + 2 * t4;
+      const float v[8] = {s_dl[warp][g][e0],         s_dl[warp][g][e0 + 1],
+                          s_dl[warp][g + 8][e0],     s_dl[warp][g + 8][e0 + 1],
+                          s_dl[warp][g][e0 + 8],     s_dl[warp][g][e0 + 9],
+                          s_dl[warp][g + 8][e0 + 8], s_dl[warp][g + 8][e0 + 9]};
 #pragma unroll
-        for (int r = 0; r < 4; ++r) {
-          const float x0 = v[2 * r], x1 = v[2 * r + 1];
-          ah[ks][r] = bf16pair(x0, x1);
-          const float h0 = __uint_as_float(ah[ks][r] << 16);
-          const float h1 = __uint_as_float(ah[ks][r] & 0xffff0000u);
-          al[ks][r] = bf16pair(x0 - h0, x1 - h1);
-        }
+      for (int r = 0; r < 4; ++r) {
+        const float x0 = v[2 * r], x1 = v[2 * r + 1];
+        ah[ks][r] = bf16pair(x0, x1);
+        const float h0 = __uint_as_float(ah[ks][r] << 16);
+        const float h1 = __uint_as_float(ah[ks][r] & 0xffff0000u);
+        al[ks][r] = bf16pair(x0 - h0, x1 - h1);
       }
     }
-    // ---- phase B: 64 columns per pass -----------------------------------------
-    for (int c0 = 0; c0 < d; c0 += 64) {
-      // issue the gathered expert-row loads first (k <= 2 fast path)
-      const int c = (c0 >> 3) + cq;
-      uint4 pre[4][2];
-      const bool fast = k <= 2;
-      if (fast) {
+    const uint4* src0[2];
+    const uint4* src1[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int ti = 4 * tq + i;
+    for (int s2 = 0; s2 < 2; ++s2) {
+      src0[s2] = (v0 && s2 < k) ? reinterpret_cast<const uint4*>(s_src[warp][g][s2]) : nullptr;
+      src1[s2] = (v1 && s2 < k) ? reinterpret_cast<const uint4*>(s_src[warp][g + 8][s2])
+                                : nullptr;
+    }
+    // ---- phase B: 64 columns (two 32-column blocks) per pass.  The gathered rows of the
+    // next kD2Stages - 1 passes are in flight as cp.async copies into this lane's own ring
+    // slots (slot j = token half * 4 + block * 2 + s; lane-private, so no warp barrier) ----
+    const int cbeg = half * dcols;
+    const int npass = dcols / 64;
+    auto issue = [&](int pass) {
+      const uint32_t st = ring + (uint32_t)((pass % kD2Stages) * 8 * 32 * 16);
+      const int c0 = (cbeg >> 3) + pass * 8 + t4;
 #pragma unroll
-          for (int s2 = 0; s2 < 2; ++s2)
-            pre[i][s2] = (ti < nt && s2 < k)
-                             ? ld_nc_v4(reinterpret_cast<const uint4*>(s_src[warp][ti][s2]) + c)
-                             : make_uint4(0, 0, 0, 0);
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          cp_async16(st + (uint32_t)((b * 2 + s2) * 512),
+                     src0[s2] ? (const void*)(src0[s2] + c0 + 4 * b) : (const void*)dx,
+                     src0[s2] != nullptr);
+          cp_async16(st + (uint32_t)((4 + b * 2 + s2) * 512),
+                     src1[s2] ? (const void*)(src1[s2] + c0 + 4 * b) : (const void*)dx,
+                     src1[s2] != nullptr);
         }
-      }
+    };
+#pragma unroll
+    for (int i = 0; i < kD2Stages - 1; ++i) {
+      if (i < npass) issue(i);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int pass = 0; pass < npass; ++pass) {
+      if (pass + kD2Stages - 1 < npass) issue(pass + kD2Stages - 1);
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      const int cb = cbeg + pass * 64;
+      const int c0 = (cb >> 3) + t4;        // chunk of block 0; block 1 is c0 + 4
+      float acc[2][4][4];
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int n = 0; n < 4; ++n)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[b][n][q] = 0.f;
       if (wg) {
-        float acc[8][4];
-#pragma unroll
-        for (int n8 = 0; n8 < 8; ++n8)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc[n8][q] = 0.f;
-        // wg is passed TRANSPOSED ([d, E], experts contiguous): each B register is one
-        // 4-byte load of two consecutive experts at one column
-        const uint32_t* wT = reinterpret_cast<const uint32_t*>(wg);
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int e0 = ks * 16 + 2 * t4;
-          uint32_t w[8][2];
 #pragma unroll
-          for (int n8 = 0; n8 < 8; ++n8) {
-            const long cbase = (long)(c0 + n8 * 8 + g) * E;
-            w[n8][0] = e0 < E ? __ldg(wT + ((cbase + e0) >> 1)) : 0u;
-            w[n8][1] = e0 + 8 < E ? __ldg(wT + ((cbase + e0 + 8) >> 1)) : 0u;
-          }
+          for (int b = 0; b < 2; ++b)
 #pragma unroll
-          for (int n8 = 0; n8 < 8; ++n8) {
-            mma16816(acc[n8], ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], w[n8][0], w[n8][1]);
-            mma16816(acc[n8], al[ks][0], al[ks][1], al[ks][2], al[ks][3], w[n8][0], w[n8][1]);
-          }
-        }
-#pragma unroll
-        for (int n8 = 0; n8 < 8; ++n8) {
-          s_rt[warp][g][n8 * 8 + 2 * t4] = acc[n8][0];
-          s_rt[warp][g][n8 * 8 + 2 * t4 + 1] = acc[n8][1];
-          s_rt[warp][g + 8][n8 * 8 + 2 * t4] = acc[n8][2];
-          s_rt[warp][g + 8][n8 * 8 + 2 * t4 + 1] = acc[n8][3];
+            for (int n = 0; n < 4; ++n) {
+              const long col = cb + b * 32 + (g >> 1) * 8 + 2 * n + (g & 1);
+              const uint32_t w0 = e0 < E ? __ldg(wT + ((col * E + e0) >> 1)) : 0u;
+              const uint32_t w1 = e0 + 8 < E ? __ldg(wT + ((col * E + e0 + 8) >> 1)) : 0u;
+              mma16816(acc[b][n], ah[ks][0], ah[ks][1], ah[ks][2], ah[ks][3], w0, w1);
+              mma16816(acc[b][n], al[ks][0], al[ks][1], al[ks][2], al[ks][3], w0, w1);
+            }
         }
       }
-      __syncwarp();
+      asm volatile("cp.async.wait_group %0;" ::"n"(kD2Stages - 1) : "memory");
+      const uint32_t st = ring + (uint32_t)((pass % kD2Stages) * 8 * 32 * 16);
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int ti = 4 * tq + i;
-        float f8[8];
-        if (wg) {
-          const float4 r0 = *reinterpret_cast<const float4*>(&s_rt[warp][ti][cq * 8]);
-          const float4 r1 = *reinterpret_cast<const float4*>(&s_rt[warp][ti][cq * 8 + 4]);
-          f8[0] = r0.x; f8[1] = r0.y; f8[2] = r0.z; f8[3] = r0.w;
-          f8[4] = r1.x; f8[5] = r1.y; f8[6] = r1.z; f8[7] = r1.w;
-        } else {
+      for (int b = 0; b < 2; ++b) {
+        float f0[8], f1[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) f8[q] = 0.f;
+        for (int n = 0; n < 4; ++n) {
+          f0[2 * n] = acc[b][n][0];
+          f0[2 * n + 1] = acc[b][n][1];
+          f1[2 * n] = acc[b][n][2];
+          f1[2 * n + 1] = acc[b][n][3];
         }
-        if (ti < nt) {
-          if (fast) {
 #pragma unroll
-            for (int s2 = 0; s2 < 2; ++s2) {
-              float f[8];
-              bf16x8_to_f32(pre[i][s2], f);
+        for (int s2 = 0; s2 < 2; ++s2) {
+          float a[8], c[8];
+          bf16x8_to_f32(ld_shared_u4(st + (uint32_t)((b * 2 + s2) * 512)), a);
+          bf16x8_to_f32(ld_shared_u4(st + (uint32_t)((4 + b * 2 + s2) * 512)), c);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) f8[q] += f[q];
+          for (int q = 0; q < 8; ++q) {
+            f0[q] += a[q];
+            f1[q] += c[q];
+          }
+        }
+        if (k > 2) {
+          for (int s2 = 2; s2 < k; ++s2) {
+            float a[8];
+            if (v0) {
+              bf16x8_to_f32(ld_nc_v4(reinterpret_cast<const uint4*>(s_src[warp][g][s2]) +
+                                     c0 + 4 * b),
+                            a);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) f0[q] += a[q];
             }
-          } else {
-            for (int s2 = 0; s2 < k; ++s2) {
-              const uint4* src = reinterpret_cast<const uint4*>(s_src[warp][ti][s2]);
-              float f[8];
-              bf16x8_to_f32(ld_nc_v4(src + c), f);
+            if (v1) {
+              bf16x8_to_f32(ld_nc_v4(reinterpret_cast<const uint4*>(s_src[warp][g + 8][s2]) +
+                                     c0 + 4 * b),
+                            a);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) f8[q] += f[q];
+              for (int q = 0; q < 8; ++q) f1[q] += a[q];
             }
           }
-          st_v4(dx + (t0 + ti) * nch + c, f32_to_bf16x8(f8));
         }
+        if (v0) st_v4(dx + (t0 + g) * nch + c0 + 4 * b, f32_to_bf16x8(f0));
+        if (v1) st_v4(dx + (t0 + g + 8) * nch + c0 + 4 * b, f32_to_bf16x8(f1));
       }
-      __syncwarp();
     }
+    __syncwarp();   // s_dl / s_src of this task consumed before the next task's phase A
   }
 }
 
@@ -572,146 +717,145 @@ __global__ void __launch_bounds__(256, 2) router_wgrad_partial(const float* __re
     part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
 }
 
-// Tensor-core variant: dWg^T[col, e] = sum_t x[t, col] dl[t, e] as mma.sync m16n8k16
-// (M = 16 columns, N = 8 experts, K = 16 tokens).  The block stages 16 tokens x 1024
-// columns of x (cp.async, double-buffered) and their dlogits; ldmatrix.trans turns the
-// token-major x tile into A fragments; dlogits enter as a bf16 hi + lo split (the
-// product keeps ~16 mantissa bits, as in the dispatch backward).  Warp w owns columns
-// [w*256, +256) of the block's slice and 16 experts (two n8 tiles).  One pass over x
-// per 16-expert group; per-block partials as in the FMA kernel.
-constexpr int kRwTok = 16, kRwCols = 1024, kRwPad = 8, kRwStages = 3;
-constexpr int kRwRow = kRwCols + kRwPad;                    // bf16 elements per smem row
-constexpr int kRwSmem = kRwStages * (kRwTok * kRwRow * 2 + kRwTok * 16 * 4);
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, bool pred) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src),
-               "r"(pred ? 16 : 0));
-}
-__global__ void __launch_bounds__(128, 2) router_wgrad_tc(const float* __restrict__ dlog,
-                                                       const __nv_bfloat16* __restrict__ x,
-                                                       int Tn, int d, int E,
-                                                       float* __restrict__ part,
-                                                       float* __restrict__ part_bias) {
-  extern __shared__ __align__(16) uint8_t rw_smem[];
+// Column-sliced tensor-core variant (the default for d % 128 == 0): block (r, c, z) reduces
+// token range r for the 128 columns [128 c, +128) and experts [16 z, +16); warp w owns 32
+// of the columns (two m16 tiles), so the accumulators are 32 registers and 8 blocks fit an
+// SM.  The token ranges are few (~8 * SMs / slices), so the partials are E * d * 4 bytes
+// per range (cfg2: 9.7 MB).  Per 16-token step the block stages 16 x 128 bf16 of x and the
+// 16 x 16 dlogits through a cp.async ring; the dlogits' hi / lo bf16 B fragments are built
+// once per step by the whole block into shared memory.
+constexpr int kR2Cols = 128, kR2Row = kR2Cols + 8, kR2Stages = 3, kR2Tok = 32;
+constexpr int kR2StageBytes = kR2Tok * kR2Row * 2 + kR2Tok * 16 * 4;   // x tile + dlogits
+constexpr int kR2Smem = kR2Stages * kR2StageBytes + (kR2Tok / 16) * 2 * 2 * 2 * 32 * 4;
+__global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restrict__ dlog,
+                                                         const __nv_bfloat16* __restrict__ x,
+                                                         int Tn, int d, int E,
+                                                         float* __restrict__ part,
+                                                         float* __restrict__ part_bias) {
+  extern __shared__ __align__(16) uint8_t r2_smem[];
   pdl_prologue();
-  __nv_bfloat16* s_x = reinterpret_cast<__nv_bfloat16*>(rw_smem);  // [stages][16][kRwRow]
-  float* s_dl = reinterpret_cast<float*>(rw_smem + kRwStages * kRwTok * kRwRow * 2);
+  constexpr int KG = kR2Tok / 16;   // 16-token k groups per step
   const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
   const int g = lane >> 2, t4 = lane & 3;
-  const int nblk = gridDim.x;
-  const int cbase = blockIdx.y * kRwCols;                 // block column slice
-  const int ncols = min(kRwCols, d - cbase);
+  const int nrange = gridDim.x;
+  const int cbase = blockIdx.y * kR2Cols;
   const int e0 = blockIdx.z * 16;
-  const long per = ((long)(Tn + nblk - 1) / nblk + kRwTok - 1) / kRwTok * kRwTok;
+  const long per = ((long)(Tn + nrange - 1) / nrange + kR2Tok - 1) / kR2Tok * kR2Tok;
   const long t_begin = (long)blockIdx.x * per;
   const long t_end = min((long)Tn, t_begin + per);
-  const uint32_t sx0 = (uint32_t)__cvta_generic_to_shared(s_x);
-  // staging assignment (computed once): thread -> 16-byte piece cc of rows ti0, +rstep, ..
-  const int pr = ncols / 8;                     // pieces per row (<= 128 = blockDim.x)
-  const int rstep = blockDim.x / pr;
-  const int ti0 = threadIdx.x < rstep * pr ? threadIdx.x / pr : kRwTok;  // idle if surplus
-  const int cc = threadIdx.x % pr;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(r2_smem);
+  // B fragments of the step: [kg][n][h][hi / lo][32 lanes]
+  uint32_t* s_bf = reinterpret_cast<uint32_t*>(r2_smem + kR2Stages * kR2StageBytes);
+  // staging: kR2Tok rows x 256 B of x (16 pieces of 16 B per row) + kR2Tok x 16 dlogits
   auto stage = [&](int buf, long tt) {
-    // x rows: 16 tokens x ncols bf16 in 16-byte pieces; dlogits 16 x 16 fp32
-    for (int ti = ti0; ti < kRwTok; ti += rstep) {
+    const uint32_t sx = sbase + (uint32_t)(buf * kR2StageBytes);
+#pragma unroll
+    for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
+      const int q = threadIdx.x + j * 128;
+      const int ti = q >> 4, cc = q & 15;
       const long t = tt + ti;
       const bool ok = t < t_end;
-      cp_async16(sx0 + (uint32_t)(((buf * kRwTok + ti) * kRwRow + cc * 8) * 2),
-                 x + (ok ? t : 0) * d + cbase + cc * 8, ok);
+      cp_async16(sx + (uint32_t)((ti * kR2Row + cc * 8) * 2), x + (ok ? t : 0) * d + cbase + cc * 8,
+                 ok);
     }
-    const uint32_t sdl0 = (uint32_t)__cvta_generic_to_shared(s_dl);
-    for (int q = threadIdx.x; q < kRwTok * 16; q += blockDim.x) {
-      const int ti = q / 16, ei = q % 16;
+    const uint32_t sdl = sx + (uint32_t)(kR2Tok * kR2Row * 2);
+#pragma unroll
+    for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
+      const int q = threadIdx.x + j * 128;
+      const int ti = q >> 4, ei = q & 15;
       const long t = tt + ti;
       const bool ok = t < t_end && e0 + ei < E;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
-                       sdl0 + (uint32_t)(((buf * kRwTok + ti) * 16 + ei) * 4)),
-                   "l"(dlog + (ok ? t * E + e0 + ei : 0)), "r"(ok ? 4 : 0));
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sdl + (uint32_t)(q * 4)),
+                   "l"(dlog + (ok ? t * E + e0 + ei : 0)), "r"(ok ? 4 : 0)
+                   : "memory");
     }
-    asm volatile("cp.async.commit_group;");
   };
-  float acc[16][2][4];
+  float acc[2][2][4];
 #pragma unroll
-  for (int m = 0; m < 16; ++m)
+  for (int m = 0; m < 2; ++m)
 #pragma unroll
     for (int n = 0; n < 2; ++n)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[m][n][q] = 0.f;
   float bacc = 0.f;
-  const int wcol = warp * 256;                            // warp's columns in the slice
-  const bool active = wcol < ncols;
-  // kRwStages-deep cp.async ring: steps i+1 .. i+kRwStages-1 are in flight while step i
-  // is consumed (one commit group per step, empty groups past the end keep the count)
-  const long nsteps = t_end > t_begin ? (t_end - t_begin + kRwTok - 1) / kRwTok : 0;
+  const long nsteps = t_end > t_begin ? (t_end - t_begin + kR2Tok - 1) / kR2Tok : 0;
 #pragma unroll
-  for (int i = 0; i < kRwStages - 1; ++i) {
-    if (i < nsteps) stage(i, t_begin + (long)i * kRwTok);
-    else asm volatile("cp.async.commit_group;");
+  for (int i = 0; i < kR2Stages - 1; ++i) {
+    if (i < nsteps) stage(i, t_begin + (long)i * kR2Tok);
+    asm volatile("cp.async.commit_group;" ::: "memory");
   }
+  // B-fragment builder roles of this thread: (n, h) = threadIdx.x / 32 for every k group
+  const int bn = threadIdx.x >> 6, bh = (threadIdx.x >> 5) & 1;
+  const int mi = lane >> 3, r = lane & 7;
   for (long i = 0; i < nsteps; ++i) {
-    const int buf = (int)(i % kRwStages);
-    const long tt = t_begin + i * kRwTok;
-    asm volatile("cp.async.wait_group %0;" ::"n"(kRwStages - 2) : "memory");
-    __syncthreads();
+    const int buf = (int)(i % kR2Stages);
+    asm volatile("cp.async.wait_group %0;" ::"n"(kR2Stages - 2) : "memory");
+    __syncthreads();   // step i landed for every thread; buffer (i - 1) % S free again
     {
-      const long j = i + kRwStages - 1;   // restage the buffer consumed at step i - 1
-      if (j < nsteps) stage((int)(j % kRwStages), t_begin + j * kRwTok);
-      else asm volatile("cp.async.commit_group;");
+      const long j = i + kR2Stages - 1;
+      if (j < nsteps) stage((int)(j % kR2Stages), t_begin + j * kR2Tok);
+      asm volatile("cp.async.commit_group;" ::: "memory");
     }
-    const float* dl = s_dl + buf * kRwTok * 16;
-    if (blockIdx.y == 0 && threadIdx.x < 16)
-      for (int ti = 0; ti < kRwTok; ++ti) bacc += dl[ti * 16 + threadIdx.x];
-    if (active) {
-      // B fragments (experts g and 8 + g; tokens 2t4, 2t4+1 and +8), hi / lo bf16
-      uint32_t bh[2][2], bl[2][2];
+    const float* dl = reinterpret_cast<const float*>(r2_smem + buf * kR2StageBytes +
+                                                     kR2Tok * kR2Row * 2);
+#pragma unroll
+    for (int kg = 0; kg < KG; ++kg) {
+      // B fragment (experts n*8 + g; tokens k0, k0 + 1 with k0 = 16 kg + 2 t4 + 8 h), hi + lo
+      const int k0 = 16 * kg + 2 * t4 + 8 * bh;
+      const float v0 = dl[k0 * 16 + bn * 8 + g], v1 = dl[(k0 + 1) * 16 + bn * 8 + g];
+      const uint32_t hi = bf16pair(v0, v1);
+      const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xffff0000u);
+      s_bf[(((kg * 2 + bn) * 2 + bh) * 2 + 0) * 32 + lane] = hi;
+      s_bf[(((kg * 2 + bn) * 2 + bh) * 2 + 1) * 32 + lane] = bf16pair(v0 - h0, v1 - h1);
+    }
+    if (blockIdx.y == 0 && threadIdx.x < 16) {
+#pragma unroll 8
+      for (int ti = 0; ti < kR2Tok; ++ti) bacc += dl[ti * 16 + threadIdx.x];
+    }
+    __syncthreads();   // B fragments of step i visible
+#pragma unroll
+    for (int kg = 0; kg < KG; ++kg) {
+      uint32_t bf[2][2][2];   // [n][h][hi / lo]
 #pragma unroll
       for (int n = 0; n < 2; ++n)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k0 = 2 * t4 + 8 * h;
-          const float v0 = dl[k0 * 16 + n * 8 + g], v1 = dl[(k0 + 1) * 16 + n * 8 + g];
-          bh[n][h] = bf16pair(v0, v1);
-          const float h0 = __uint_as_float(bh[n][h] << 16);
-          const float h1 = __uint_as_float(bh[n][h] & 0xffff0000u);
-          bl[n][h] = bf16pair(v0 - h0, v1 - h1);
-        }
-      // A fragments: ldmatrix.x4.trans of the 16 tokens x 16 columns submatrix
-      const int mi = lane >> 3, r = lane & 7;
-      const uint32_t abase = sx0 + (uint32_t)(((buf * kRwTok + (mi >> 1) * 8 + r) * kRwRow +
-                                               wcol + (mi & 1) * 8) * 2);
+        for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        if (wcol + m * 16 >= ncols) break;
+          for (int hl = 0; hl < 2; ++hl)
+            bf[n][h][hl] = s_bf[(((kg * 2 + n) * 2 + h) * 2 + hl) * 32 + lane];
+      // A fragments: ldmatrix.x4.trans of the 16 tokens x 16 columns submatrix
+      const uint32_t abase =
+          sbase + (uint32_t)(buf * kR2StageBytes) +
+          (uint32_t)(((16 * kg + (mi >> 1) * 8 + r) * kR2Row + warp * 32 + (mi & 1) * 8) * 2);
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
         uint32_t a0, a1, a2, a3;
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
                      : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
                      : "r"(abase + m * 32));
 #pragma unroll
         for (int n = 0; n < 2; ++n) {
-          mma16816(acc[m][n], a0, a1, a2, a3, bh[n][0], bh[n][1]);
-          mma16816(acc[m][n], a0, a1, a2, a3, bl[n][0], bl[n][1]);
+          mma16816(acc[m][n], a0, a1, a2, a3, bf[n][0][0], bf[n][1][0]);
+          mma16816(acc[m][n], a0, a1, a2, a3, bf[n][0][1], bf[n][1][1]);
         }
       }
     }
-    (void)tt;
   }
-  // partial[blk][e][col]: C fragment rows = columns (g, g + 8), cols = experts (2t4, +1)
-  if (active) {
-    float* pb = part + (long)blockIdx.x * E * d;
+  // partial[range][e][col]: C fragment rows = columns (g, g + 8), cols = experts (2t4, +1)
+  float* pb = part + (long)blockIdx.x * E * d;
 #pragma unroll
-    for (int m = 0; m < 16; ++m) {
-      const int c = cbase + wcol + m * 16 + g;
-      if (wcol + m * 16 >= ncols) break;
+  for (int m = 0; m < 2; ++m) {
+    const int c = cbase + warp * 32 + m * 16 + g;
 #pragma unroll
-      for (int n = 0; n < 2; ++n) {
-        const int e = e0 + n * 8 + 2 * t4;
-        if (e < E) {
-          pb[(long)e * d + c] = acc[m][n][0];
-          pb[(long)e * d + c + 8] = acc[m][n][2];
-        }
-        if (e + 1 < E) {
-          pb[(long)(e + 1) * d + c] = acc[m][n][1];
-          pb[(long)(e + 1) * d + c + 8] = acc[m][n][3];
-        }
+    for (int n = 0; n < 2; ++n) {
+      const int e = e0 + n * 8 + 2 * t4;
+      if (e < E) {
+        pb[(long)e * d + c] = acc[m][n][0];
+        pb[(long)e * d + c + 8] = acc[m][n][2];
+      }
+      if (e + 1 < E) {
+        pb[(long)(e + 1) * d + c] = acc[m][n][1];
+        pb[(long)(e + 1) * d + c + 8] = acc[m][n][3];
       }
     }
   }
@@ -930,6 +1074,16 @@ extern "C" lz_status lz_combine_bwd_p2p_ret(const void* dout, const void* y_ret,
                           own_dy, dw, E, recv_m, recv_off, stream, y_row);
 }
 
+template <int KS, int ET>
+static void d2_attr() {
+  static bool done = false;   // one per instantiation
+  if (!done) {
+    cudaFuncSetAttribute(dispatch_bwd_reg<KS, ET>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kD2Smem);
+    done = true;
+  }
+}
+
 static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const int32_t* prank,
                                    const unsigned long long* peers, int Tn, int d, int k,
                                    const float* probs, const int32_t* idx, const float* dw,
@@ -941,13 +1095,16 @@ static lz_status dispatch_bwd_impl(const void* dxe, const int32_t* row, const in
   if ((!dxe && !peers) || !row || !probs || !idx || !dw || !dx || !dlogits) return LZ_ERR_ARG;
   if (d % 64 || E % 2) return LZ_ERR_UNSUPPORTED;
   const long dtasks = (Tn + kDT - 1) / kDT;
-  long dgrid = (dtasks + kDWarps - 1) / kDWarps;
-  const long dcap = (long)lzh::num_sms() * 16;
-  if (dgrid > dcap) dgrid = dcap;
+  const int nh = (d % 128 == 0) ? 2 : 1;   // column halves per 16-token tile (load balance)
+  // persistent: as many blocks as are resident (4 per SM)
+  long dgrid = (dtasks * nh + kD2Warps - 1) / kD2Warps;
+  const long cap = (long)lzh::num_sms() * LZ_D2_BLOCKS;
+  if (dgrid > cap) dgrid = cap;
 #define LZ_DBWD(ks, et)                                                                      \
-  lzh::launch(dispatch_bwd_kernel<ks, et>, dim3((int)dgrid), dim3(32 * kDWarps), 0,             \
-              (cudaStream_t)stream, 1, (const uint4*)dxe, row, prank, peers, Tn, d, k, probs,   \
-              idx, dw, (const __nv_bfloat16*)wg, E, renorm, (uint4*)dx, dlogits)
+  (d2_attr<ks, et>(),                                                                        \
+   lzh::launch(dispatch_bwd_reg<ks, et>, dim3((int)dgrid), dim3(32 * kD2Warps), kD2Smem,       \
+               (cudaStream_t)stream, 1, (const uint4*)dxe, row, prank, peers, Tn, d, k, probs,  \
+               idx, dw, (const __nv_bfloat16*)wg, E, renorm, (uint4*)dx, dlogits, nh))
   switch (E) {
     case 8: LZ_DBWD(1, 8); break;
     case 16: LZ_DBWD(1, 16); break;
@@ -986,12 +1143,14 @@ extern "C" lz_status lz_dispatch_bwd_p2p(const unsigned long long* peers_dxe,
 
 // tensor-core path: d a multiple of 256 (whole warp column blocks); one block per SM
 // per (column slice, expert group); else the FMA path with 2 blocks per SM
-static bool wgrad_tc(int d) { return d % 256 == 0; }
+// tensor-core path: d a multiple of 128 (column slices of 128); ~8 blocks per SM over
+// (token range, column slice, expert group); else the FMA path with 2 blocks per SM
+static bool wgrad_tc(int d) { return d % kR2Cols == 0; }
 static int wgrad_nblk(int Tn, int d, int E) {
   if (wgrad_tc(d)) {
-    const int slices = ((d + kRwCols - 1) / kRwCols) * ((E + 15) / 16);
-    int n = (2 * lzh::num_sms() + slices - 1) / slices;  // 2 blocks per SM
-    const int steps = (Tn + kRwTok - 1) / kRwTok;
+    const int slices = (d / kR2Cols) * ((E + 15) / 16);
+    int n = (6 * lzh::num_sms() + slices - 1) / slices;
+    const int steps = (Tn + kR2Tok - 1) / kR2Tok;
     if (n > steps) n = steps;
     return n < 1 ? 1 : n;
   }
@@ -1022,15 +1181,8 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
   float* part = (float*)ws;
   float* part_bias = part + (size_t)nblk * E * d;
   if (wgrad_tc(d)) {
-    static bool attr = false;
-    if (!attr) {
-      if (cudaFuncSetAttribute(router_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               kRwSmem) != cudaSuccess)
-        return lzh::check_launch();
-      attr = true;
-    }
-    dim3 grid(nblk, (d + kRwCols - 1) / kRwCols, (E + 15) / 16);
-    lzh::launch(router_wgrad_tc, grid, dim3(128), kRwSmem, s, 1, dlogits,
+    dim3 grid(nblk, d / kR2Cols, (E + 15) / 16);
+    lzh::launch(router_wgrad_tc2, grid, dim3(128), kR2Smem, s, 1, dlogits,
                 (const __nv_bfloat16*)x, Tn, d, E, part, part_bias);
   } else {
     dim3 grid(nblk, (d + 1023) / 1024, (E + kWgE - 1) / kWgE);
