@@ -1133,11 +1133,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             continue;
           }
-          // the store that used buffer b (chunk c-2) must have finished reading smem
-          if (lane == 0) bulk_wait_read<1>();
-          __syncwarp();
+          // GELU: y and gelu'(y) in registers first; the aux stores are issued only AFTER
+          // this chunk's smem staging + proxy fence + TMA store, so the fence (which orders
+          // this thread's earlier generic-proxy writes) never waits for them
+          uint4 auxv[4];
           if constexpr (K == 1) {
-            uint4* aux_wr = aux_block(p, p.N, row0, col0 + c * kEpiCols) + lane;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               float dg[8];
@@ -1150,9 +1150,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 dg[i] = d2.x;
                 dg[i + 1] = d2.y;
               }
-              st_v4(aux_wr + q * 32, f32_to_bf16x8(dg));
+              auxv[q] = f32_to_bf16x8(dg);
             }
           }
+          // the store that used buffer b (chunk c-2) must have finished reading smem
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             st_shared_v4(out_s + b * kEpiBuf + stg_off(lane, q), f32_to_bf16x8(f + 8 * q));
@@ -1161,6 +1164,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (lane == 0) {
             tma_store_2d(smap, wbuf + b * kEpiBuf, col0 + c * kEpiCols, srow);
             bulk_commit();
+          }
+          if constexpr (K == 1) {
+            uint4* aux_wr = aux_block(p, p.N, row0, col0 + c * kEpiCols) + lane;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st_v4(aux_wr + q * 32, auxv[q]);
           }
         }
       };

@@ -125,7 +125,8 @@ def multilayer(group, n_layers=4):
     h = run_step(layers, step)
     retries = len(runs) - 1
     peak = torch.cuda.max_memory_allocated() / 2**30
-    rows = [L._symm.rows for L in layers]
+    # symmetric exchange buffers exist only with the P2P exchange (LZ_EXCHANGE=nccl: none)
+    rows = [L._symm.rows if L._symm is not None else None for L in layers]
     print(f"[{n_layers} layers N={n}] rank {dist.get_rank(group)} exchange rows {rows} "
           f"(N*Tn*k = {n * Tn * k}), capacity re-runs {retries}, peak memory {peak:.1f} GiB",
           flush=True)
