@@ -133,6 +133,14 @@ __device__ __forceinline__ void pdl_prologue() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
+// The two halves, for kernels with a prologue that touches no global memory a predecessor
+// may write (barrier init, TMEM allocation, staging of weights no kernel of the chain
+// writes): launch_dependents first, the prologue, then wait before any other global
+// access -- the prologue overlaps the predecessor's tail.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll

@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
   __shared__ __align__(8) uint64_t full_bar[kGsStages], empty_bar[kGsStages];
   __shared__ __align__(8) uint64_t tfull_bar[kGsTiles], tempty_bar[kGsTiles];
   __shared__ int32_t s_hist[16];
-  pdl_prologue();
+  pdl_launch_dependents();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int rowb = (d + 8) * 2;                    // padded smem row, bytes
   uint8_t* ring = gs_smem;                         // [stages][16][d + 8] bf16
@@ -543,9 +543,6 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
           : "memory");
   };
   const bool producer = warp == kGsMma + kGsFin;
-  // the first ring stages are in flight before the router weights are staged
-  if (producer)
-    for (int i = 0; i < kGsStages && g_begin + i < g_end; ++i) issue(g_begin + i, i);
   {
     // router weights -> smem (rows >= E zero), every thread's loads in flight at once
     constexpr int kPer = (16 * 1024 / 8 + kGsThreads - 1) / kGsThreads;   // d <= 1024
@@ -566,6 +563,10 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
   }
   __syncthreads();
   if (producer) {
+    // the barrier init and the router-weight staging above overlap the predecessor's tail
+    // (PDL; no kernel of the step writes wg); x and every output only after the wait
+    pdl_wait();
+    for (int i = 0; i < kGsStages && g_begin + i < g_end; ++i) issue(g_begin + i, i);
     for (int gi = g_begin + kGsStages, i = kGsStages; gi < g_end; ++gi, ++i) {
       gs_wait(&empty_bar[i % kGsStages], ((i / kGsStages) - 1) & 1);
       issue(gi, i);

@@ -756,13 +756,50 @@ __global__ void __launch_bounds__(kThreads, 1)
   int32_t* s_off = (int32_t*)((uint8_t*)full_bar + kBarBytes);
   int32_t* s_pref = s_off + kMaxGroups + 1;
 
-  pdl_prologue();
+  pdl_launch_dependents();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t cta = CG == 1 ? 0u : cluster_ctarank();
   const bool leader = cta == 0;
   const int unit = CG == 1 ? blockIdx.x : (blockIdx.x >> 1);   // tile-processing unit
   const int nunits = CG == 1 ? gridDim.x : (gridDim.x >> 1);
 
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull_bar[s], 1);
+      mbar_init(&tempty_bar[s], kEpiWarps * CG);  // one arrival per epilogue warp of each CTA
+    }
+    for (int s = 0; s < kSchedSlots; ++s) {
+      mbar_init(&sched_full[s], 1);
+      // read by: the MMA warp and every epilogue warp of the leader, the peer's producer and
+      // every epilogue warp of the peer
+      mbar_init(&sched_empty[s], CG == 1 ? 1 + kEpiWarps : 2 + 2 * kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
+    if (p.epilogue != LZ_EPI_STORE) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
+  }
+  if (warp == 1) {
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(s_tmem)),
+                   "r"(kTmemCols));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  // barrier init, tensor-map prefetch and TMEM allocation above overlap the predecessor's
+  // tail (PDL); the device offsets and every operand only after the wait
+  pdl_wait();
   // group table -> tile prefix (every CTA computes it; G <= kMaxGroups).  Weight-gradient
   // groups are visited in descending K (tile cost); row GEMM tiles all cost the same.
   int32_t* s_perm = s_pref + kMaxGroups + 1;
@@ -807,40 +844,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     s_pref[p.G] = acc;
     *s_total0 = acc0;
-  }
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full_bar[s], 1);
-      mbar_init(&empty_bar[s], 1);
-    }
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&tfull_bar[s], 1);
-      mbar_init(&tempty_bar[s], kEpiWarps * CG);  // one arrival per epilogue warp of each CTA
-    }
-    for (int s = 0; s < kSchedSlots; ++s) {
-      mbar_init(&sched_full[s], 1);
-      // read by: the MMA warp and every epilogue warp of the leader, the peer's producer and
-      // every epilogue warp of the peer
-      mbar_init(&sched_empty[s], CG == 1 ? 1 + kEpiWarps : 2 + 2 * kEpiWarps);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_c) : "memory");
-    if (p.epilogue != LZ_EPI_STORE) asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
-  }
-  if (warp == 1) {
-    if (CG == 1) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(s_tmem)),
-                   "r"(kTmemCols));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       smem_u32(s_tmem)),
-                   "r"(kTmemCols));
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
-    }
   }
   tc_fence_before();
   if (CG == 1) __syncthreads();
