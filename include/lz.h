@@ -153,6 +153,13 @@ lz_status lz_router_gate(const void* x, const void* wg, const float* bias, int T
                          int k, int renorm, int32_t* idx, float* w, float* probs, int32_t* hist,
                          void* stream);
 
+/* Gate backward alone: dlogits[Tn, E] (fp32) from probs (fp32 [Tn, E]), idx and the
+ * combine backward's dw [Tn, k] -- softmax + top-k (+ renorm) backward,
+ * bit-identical to the dlogits lz_dispatch_bwd returns.  Lets the router weight gradient
+ * start right after the combine backward.  probs / dlogits 16-byte aligned. */
+lz_status lz_gate_bwd(const float* probs, const int32_t* idx, const float* dw, int Tn, int E,
+                      int k, int renorm, float* dlogits, void* stream);
+
 /* Replaces invert_permutation (dispatch.py:240-244): out[index[i]] = i. */
 lz_status lz_invert_permutation(const int32_t* index, int n, int32_t* out, void* stream);
 

@@ -46,6 +46,7 @@ _SIGS = {
                                 _i, _vp],
     "lz_gate_topk": [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
     "lz_router_gate": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _vp],
+    "lz_gate_bwd": [_vp, _vp, _vp, _i, _i, _i, _i, _vp, _vp],
     "lz_invert_permutation": [_vp, _i, _vp, _vp],
     "lz_pack": [_vp, _i, _i, _i, _vp, _vp, _i, _vp, _vp, _vp],
     "lz_copy_segments": [_vp, _vp, _i, _i, _vp, _vp, _vp, _i, _vp],
@@ -104,7 +105,7 @@ def exported_symbols() -> list[str]:
 
 # kernels each entry point launches (for the bench's gpu_launches count)
 _KERNELS = {"lz_plan_matrices": 1, "lz_plan_dispatch": 3, "lz_shuffle_index": 3,
-            "lz_gate_topk": 1, "lz_router_gate": 1, "lz_invert_permutation": 1, "lz_pack": 1,
+            "lz_gate_topk": 1, "lz_router_gate": 1, "lz_gate_bwd": 1, "lz_invert_permutation": 1, "lz_pack": 1,
             "lz_copy_segments": 1, "lz_combine": 1, "lz_combine_bwd": 1, "lz_dispatch_bwd": 1,
             "lz_router_wgrad": 2, "lz_grouped_gemm": 1, "lz_pack_p2p": 1, "lz_combine_p2p": 1,
             "lz_combine_bwd_p2p": 1, "lz_dispatch_bwd_p2p": 1, "lz_load_record": 1,

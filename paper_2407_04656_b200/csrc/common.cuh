@@ -142,6 +142,44 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Softmax / top-k (/ renorm) backward of one token (the gate backward):
+// with the k routed ids' probabilities ps and upstream weight gradients g (= dw),
+//   renorm: g_s <- (g_s - sum_s' g_s' ps_s' / S) / S,  S = sum_s ps_s
+//   dot = sum_s g_s ps_s,   dlogits_e = -p_e dot + sum_s [e == id_s] ps_s g_s.
+// Returns dot and turns g into the coefficients c_s = ps_s g_s.  Explicit roundings, so
+// every kernel that evaluates it (lz_gate_bwd, lz_dispatch_bwd) gets identical bits.
+__device__ __forceinline__ float gate_bwd_coefs(int k, int renorm, const float* ps, float* g) {
+  float S = 0.f;
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s)
+    if (s < k) S = __fadd_rn(S, ps[s]);
+  if (renorm) {
+    float sdw = 0.f;
+#pragma unroll
+    for (int s = 0; s < LZ_MAX_TOPK; ++s)
+      if (s < k) sdw = __fmaf_rn(g[s], __fdiv_rn(ps[s], S), sdw);
+#pragma unroll
+    for (int s = 0; s < LZ_MAX_TOPK; ++s)
+      if (s < k) g[s] = __fdiv_rn(__fsub_rn(g[s], sdw), S);
+  }
+  float dot = 0.f;
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s)
+    if (s < k) dot = __fmaf_rn(g[s], ps[s], dot);
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s) g[s] = s < k ? __fmul_rn(ps[s], g[s]) : 0.f;
+  return dot;
+}
+// dlogits_e of expert e from gate_bwd_coefs' results (ids of unused slots are -1)
+__device__ __forceinline__ float gate_bwd_dl(float p_e, int e, float dot, const int* ids,
+                                             const float* c) {
+  float v = __fmul_rn(-p_e, dot);
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s)
+    if (ids[s] == e) v = __fadd_rn(v, c[s]);
+  return v;
+}
+
 __device__ __forceinline__ float warp_max(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));

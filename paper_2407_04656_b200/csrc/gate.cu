@@ -646,9 +646,58 @@ __host__ __device__ constexpr size_t gs_smem_bytes(int d) {
          (size_t)kGsTiles * kGsMma * 16 * kGsEP * sizeof(float);
 }
 
+// Gate backward alone (thread per token): dlogits from probs, idx and the combine
+// backward's dw -- the values lz_dispatch_bwd also produces (same gate_bwd_coefs), available
+// right after the combine backward, so the router weight gradient can start there.
+__global__ void __launch_bounds__(256) gate_bwd_kernel(const float* __restrict__ probs,
+                                                       const int32_t* __restrict__ idx,
+                                                       const float* __restrict__ dw, int Tn,
+                                                       int E, int k, int renorm,
+                                                       float* __restrict__ dlogits) {
+  pdl_prologue();
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= Tn) return;
+  int ids[LZ_MAX_TOPK];
+  float ps[LZ_MAX_TOPK], g[LZ_MAX_TOPK];
+#pragma unroll
+  for (int s = 0; s < LZ_MAX_TOPK; ++s) {
+    ids[s] = -1;
+    ps[s] = g[s] = 0.f;
+    if (s < k) {
+      ids[s] = __ldg(idx + t * k + s);
+      g[s] = __ldg(dw + t * k + s);
+      ps[s] = __ldg(probs + t * E + ids[s]);
+    }
+  }
+  const float dot = gate_bwd_coefs(k, renorm, ps, g);
+  const float* pr = probs + t * E;
+  float* out = dlogits + t * E;
+  if (E % 4 == 0) {
+    for (int e = 0; e < E; e += 4) {
+      const float4 p4 = __ldg(reinterpret_cast<const float4*>(pr + e));
+      *reinterpret_cast<float4*>(out + e) =
+          make_float4(gate_bwd_dl(p4.x, e, dot, ids, g), gate_bwd_dl(p4.y, e + 1, dot, ids, g),
+                      gate_bwd_dl(p4.z, e + 2, dot, ids, g), gate_bwd_dl(p4.w, e + 3, dot, ids, g));
+    }
+  } else {
+    for (int e = 0; e < E; ++e) out[e] = gate_bwd_dl(__ldg(pr + e), e, dot, ids, g);
+  }
+}
+
 }  // namespace lz
 
 using namespace lz;
+
+extern "C" lz_status lz_gate_bwd(const float* probs, const int32_t* idx, const float* dw, int Tn,
+                                 int E, int k, int renorm, float* dlogits, void* stream) {
+  if (Tn < 0 || E < 1 || E > LZ_MAX_EXPERTS || k < 1 || k > LZ_MAX_TOPK || k > E) return LZ_ERR_ARG;
+  if (Tn == 0) return LZ_OK;
+  if (!probs || !idx || !dw || !dlogits) return LZ_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(probs) | reinterpret_cast<uintptr_t>(dlogits)) % 16)
+    return LZ_ERR_ARG;
+  return lzh::launch(gate_bwd_kernel, dim3((Tn + 255) / 256), dim3(256), 0, (cudaStream_t)stream,
+                     1, probs, idx, dw, Tn, E, k, renorm, dlogits);
+}
 
 extern "C" lz_status lz_gate_topk(const float* logits, int Tn, int E, int k, int renorm,
                                   int32_t* idx, float* w, float* probs, int32_t* hist,

@@ -429,7 +429,6 @@ __global__ void __launch_bounds__(32 * kD2Warps) dispatch_bwd_reg(
       if (t < Tn) {
         int ids[LZ_MAX_TOPK];
         float gs[LZ_MAX_TOPK], ps[LZ_MAX_TOPK];
-        float S = 0.f;
 #pragma unroll
         for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2) {
           ids[s2] = -1;
@@ -452,33 +451,14 @@ __global__ void __launch_bounds__(32 * kD2Warps) dispatch_bwd_reg(
           }
           ids[s2] = e;
           ps[s2] = p;
-          S += p;
           if (h == 0) {
             const uint4* base = peers ? reinterpret_cast<const uint4*>(peers[rk]) : dxe;
             s_src[warp][ti][s2] = (long long)(base + (long)rr * nch);
           }
         }
-        if (renorm) {
-          float sdw = 0.f;
+        const float dot = gate_bwd_coefs(k, renorm, ps, gs);
 #pragma unroll
-          for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
-            if (s2 < k) sdw += gs[s2] * (ps[s2] / S);
-#pragma unroll
-          for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
-            if (s2 < k) gs[s2] = (gs[s2] - sdw) / S;
-        }
-        float dot = 0.f;
-#pragma unroll
-        for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2)
-          if (s2 < k) dot += gs[s2] * ps[s2];
-#pragma unroll
-        for (int j = 0; j < EH; ++j) dl[j] = -in.pr[j] * dot;
-#pragma unroll
-        for (int s2 = 0; s2 < LZ_MAX_TOPK; ++s2) {
-#pragma unroll
-          for (int j = 0; j < EH; ++j)
-            if (ids[s2] == h * EH + j) dl[j] += ps[s2] * gs[s2];
-        }
+        for (int j = 0; j < EH; ++j) dl[j] = gate_bwd_dl(in.pr[j], h * EH + j, dot, ids, gs);
         if (half == 0) {
           if (ET > 0 && ET % 8 == 0 && EH % 4 == 0) {
 #pragma unroll

@@ -135,6 +135,12 @@ class MoELayer(torch.nn.Module):
         # graph replay 6.12 -> 6.04 ms/step at N = 1, tools/tail_ab.py)
         self.tail_overlap = os.environ.get("LZ_TAIL_OVERLAP", "1") != "0"
         self.tail_overlap_nx = os.environ.get("LZ_TAIL_OVERLAP_NX", "0") == "1"   # N > 1
+        # without the tail overlap (N > 1 default), LZ_EARLY_RWGRAD=1: the gate backward right
+        # after the combine backward (lz_gate_bwd) and the router weight gradient on a side
+        # stream from there (it needs only dlogits and x).  Bit-identical gradients; same-box
+        # A/B at N = 2 (tools/step_ab.py): 7.07 vs 7.16 and 7.10 vs 7.06 ms/step -- within
+        # noise (the side kernel only gets SMs in the persistent GEMMs' tails), so off
+        self.early_router_wgrad = os.environ.get("LZ_EARLY_RWGRAD", "0") == "1"
         self._tail_stream = None
         # exchange buffers: rows = slack x this rank's assignments (+ expert padding); the
         # planner detects a larger need on the device and reserve() grows them
@@ -477,6 +483,20 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
                           max_seg)
         del dret, stage
     _mark(layer, "combine_bwd")
+    main = torch.cuda.current_stream(dev)
+    tail = layer.tail_overlap and (mode == "local" or (scatter and layer.tail_overlap_nx))
+    early = layer.early_router_wgrad and not tail
+    side = None
+    if early:
+        if layer._tail_stream is None:
+            layer._tail_stream = torch.cuda.Stream(dev)
+        side = layer._tail_stream
+        dlog_e = ops.gate_bwd(probs, idx, dw, layer.renorm)
+        side.wait_stream(main)
+        _mark(layer, "side_start", side)
+        with torch.cuda.stream(side):
+            dwg, dbg = ops.router_wgrad(dlog_e, x)
+        _mark(layer, "router_wgrad", side)
     swi = layer.activation == "swiglu"
     dH = torch.empty_like(H)
     dW1 = torch.empty_like(w1)
@@ -485,13 +505,11 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
     # while the replica-group all-reduces of the weight gradients run on NCCL's streams,
     # the GEMMs next to them leave `overlap_reserve` SMs free
     ov = max(2, (lzh_num_sms() - layer.overlap_reserve)) if N > 1 else 0
-    main = torch.cuda.current_stream(dev)
     # tail overlap (N = 1): dX GEMM right after the dgrad GEMM; the dispatch backward +
     # router weight gradient (they need only dX, dw and the gate state) then run on a side
     # stream under the two weight-gradient GEMMs.  N > 1 keeps the dX GEMM last: it hides
     # the all-reduce of the last expert gradient (~0.33 ms at cfg2, N = 2), which the tail
     # overlap would expose instead (measured 6.57 vs ~6.1 ms/step at N = 2).
-    tail = layer.tail_overlap and (mode == "local" or (scatter and layer.tail_overlap_nx))
     if G > 0:
         # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H); on N > 1 the
         # tiles of our own rows start while the other ranks' dY rows arrive
@@ -502,7 +520,6 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
             ops.grouped_gemm_rows(dY, w2, off, dH, b_major=_lib.LZ_MN_MAJOR, aux=H,
                                   epilogue=epi2)
     works = []
-    side = None
     if tail:
         if G > 0:
             # dX = dH . W1 (W1_e [d_ff, d] read MN-major); scatter: rows go back to their
@@ -567,8 +584,14 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
             yield (A2A, dxe, dXst, send_sizes, recv_counts)
             dx, dlog = ops.dispatch_bwd(dxe, row, probs, idx, dw, wg, layer.renorm, Tn)
         _mark(layer, "dispatch_bwd")
-        dwg, dbg = ops.router_wgrad(dlog, x)
-        _mark(layer, "router_wgrad")
+        if early:
+            main.wait_stream(side)
+            for t_ in (dwg, dbg, dlog_e):
+                if t_ is not None:
+                    t_.record_stream(main)
+        else:
+            dwg, dbg = ops.router_wgrad(dlog, x)
+            _mark(layer, "router_wgrad")
     if N > 1:
         yield (WAIT, works)
         flat = torch.cat([dwg.view(-1), dbg])

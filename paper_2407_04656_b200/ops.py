@@ -120,6 +120,18 @@ def dispatch_bwd(dxe, row, probs, idx, dw, wg, renorm: bool, Tn: int):
     return dx, dlog
 
 
+def gate_bwd(probs, idx, dw, renorm: bool):
+    """dlogits [Tn, E] of the gate (softmax / top-k backward) -- bit-identical to the
+    dlogits dispatch_bwd returns, available right after the combine backward."""
+    _cuda(probs, idx, dw)
+    Tn, E = probs.shape
+    k = idx.shape[1]
+    dlog = torch.empty((Tn, E), dtype=torch.float32, device=probs.device)
+    _lib.call("lz_gate_bwd", ptr(probs), ptr(idx), ptr(dw), Tn, E, k, int(renorm), ptr(dlog),
+              _s())
+    return dlog
+
+
 def router_wgrad(dlogits, x, with_bias: bool = True):
     _cuda(dlogits, x)
     Tn, d = x.shape

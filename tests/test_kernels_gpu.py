@@ -141,6 +141,10 @@ def test_dispatch_bwd_and_router_grads(renorm, Tn, d, E, k):
     dx, dlog = ops.dispatch_bwd(dxe.cuda(), row.cuda(), probs.detach().cuda(), idx.cuda(),
                                 dw.cuda(), wg.cuda(), renorm, Tn)
     _close(dlog, ref_dlog, rtol=1e-4, atol_scale=1e-5)
+    # the gate backward alone (router weight gradient off the critical path) gives the
+    # same bits as the fused dispatch backward
+    dlog2 = ops.gate_bwd(probs.detach().cuda(), idx.cuda(), dw.cuda(), renorm)
+    assert torch.equal(dlog2, dlog)
     ref_dx = dxe.float()[row.long()].view(Tn, k, d).sum(1) + ref_dlog @ wg.float()
     _close(dx, ref_dx)
     dwg, db = ops.router_wgrad(dlog, x.cuda())
