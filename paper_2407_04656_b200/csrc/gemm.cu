@@ -45,15 +45,23 @@ constexpr int kTabBytes = 3 * (kMaxGroups + 1) * 4;  // s_off, s_pref, s_perm
 // the plain-store variant carries none of the activation code).  Aux streams bypass
 // shared memory (aux_block), so every variant stages only its outputs: 2 x 2 KB per
 // epilogue warp, leaving room for 6 (CTA pair) / 4 (single CTA) operand stages.
-template <int CG, bool AUX>
+// NS = 2 (CTA pair, weight-gradient GEMMs): a 256 x 512 tile as two 256-column UMMAs per
+// k step sharing the A stage -- the A operand is read from L2 once per 512 output columns
+// (L2 -> SM operand traffic -25 %).  Its 512 accumulator columns fill TMEM, so there is one
+// accumulator (the epilogue of tile i is not overlapped with the main loop of tile i + 1;
+// with the weight gradients' long K that costs ~2 % and the GEMMs are L2-bound).
+template <int CG, bool AUX, int NS = 1>
 struct Cfg {
   static constexpr int kEpiWarpBytes = 2 * kEpiBuf;
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
-  static constexpr int kBRows = BN / CG;                 // B rows (n) staged per CTA
+  static constexpr int kTileN = BN * NS;                 // output columns per tile
+  static constexpr int kBRows = BN / CG;                 // B rows (n) per sub-tile per CTA
   static constexpr int kATileBytes = BM * BK * 2;        // 16 KB
-  static constexpr int kBTileBytes = kBRows * BK * 2;    // 32 KB / 16 KB
+  static constexpr int kBSubBytes = kBRows * BK * 2;     // 32 KB / 16 KB per sub-tile
+  static constexpr int kBTileBytes = NS * kBSubBytes;
   static constexpr int kStageBytes = kATileBytes + kBTileBytes;
-  static constexpr int kStages = CG == 1 ? 4 : 6;
+  static constexpr int kStages = CG == 1 ? 4 : (NS == 1 ? 6 : 4);
+  static constexpr int kNAcc = NS == 1 ? 2 : 1;          // TMEM accumulator buffers
   static constexpr int kTilesBytes = kStages * kStageBytes;
   static constexpr int kTileM = BM * CG;                 // rows per (pair) tile
   static constexpr int kSmemBytes = 1024 + kTilesBytes + kEpiBytes + kBarBytes + kTabBytes;
@@ -468,16 +476,16 @@ struct TileInfo {
 template <int CG>
 __host__ __device__ constexpr int C_TILE_M() { return BM * CG; }
 
-template <int CG>
+template <int CG, int NS = 1>
 __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* s_pref,
                                                 const int32_t* s_off, const int32_t* s_perm,
                                                 int total0, int tile) {
-  // (tiles are TileM x BN; mb counts TileM blocks).
+  // (tiles are TileM x BN*NS; mb counts TileM blocks, nb tile-wide column blocks).
   // mode 1: tiles numbered over the groups in s_perm order (descending K).
   // mode 0: class-0 tiles (fully inside a group's self rows, count s_perm[g] >> 16 m-blocks
   //         from m-block s_perm[g] & 0xffff) come first, then the class-1 rest in group
   //         order (prefix s_pref); without self rows class 0 is empty.
-  const int nbn = p.N / BN;
+  const int nbn = p.N / (BN * NS);
   TileInfo t;
   t.remote = false;
   // mode 0: B slices (K x 256 weights per n-block) are the re-read operand
@@ -732,14 +740,15 @@ __device__ __forceinline__ void swiglu_epilogue(const Params& p, bool fwd, const
   }
 }
 
-template <int A_MN, int B_MN, int CG, bool AUX>
+template <int A_MN, int B_MN, int CG, bool AUX, int NS>
 __global__ void __launch_bounds__(kThreads, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                         const __grid_constant__ CUtensorMap map_b,
                         const __grid_constant__ CUtensorMap map_c,
                         const __grid_constant__ CUtensorMap map_x, const Params p,
                         const __grid_constant__ RetMaps rmaps) {
-  using C = Cfg<CG, AUX>;
+  using C = Cfg<CG, AUX, NS>;
+  static_assert(NS == 1 || (CG == 2 && !AUX), "256 x 512 tiles: CTA pair, store epilogue");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* s_tiles = smem;
@@ -831,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (threadIdx.x == 0) {
     int acc = 0, acc0 = 0;
-    const int nbn = p.N / BN;
+    const int nbn = p.N / C::kTileN;
     for (int i = 0; i < p.G; ++i) {
       s_pref[i] = acc;
       if (p.mode == 0) {
@@ -940,7 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       bool arrived = p.flags == nullptr;
       for (int tile = next_tile(leader); tile < total; tile = next_tile(leader)) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
+        const TileInfo t = decode_tile<CG, NS>(p, s_pref, s_off, s_perm, total0, tile);
         if (t.remote && !arrived) {   // first tile with rows from other ranks
           wait_arrivals(p);
           arrived = true;
@@ -953,14 +962,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (p.mode == 0) {
             const int row = s_off[t.g] + t.mb * C::kTileM + cta * BM;
             load_a<A_MN, CG>(&map_a, sa, &full_bar[stage], row, 0, kb * BK);
-            load_b<B_MN, CG>(&map_b, sb, &full_bar[stage],
-                             t.g * p.N + t.nb * BN + cta * C::kBRows,
-                             t.nb * BN + cta * C::kBRows, t.g * p.K + kb * BK, kb * BK);
+#pragma unroll
+            for (int j = 0; j < NS; ++j) {
+              const int n0 = t.nb * C::kTileN + j * BN + cta * C::kBRows;
+              load_b<B_MN, CG>(&map_b, sb + j * C::kBSubBytes, &full_bar[stage], t.g * p.N + n0,
+                               n0, t.g * p.K + kb * BK, kb * BK);
+            }
           } else {
             const int krow = s_off[t.g] + kb * BK;
             load_a<A_MN, CG>(&map_a, sa, &full_bar[stage], krow, t.mb * C::kTileM + cta * BM, 0);
-            load_b<B_MN, CG>(&map_b, sb, &full_bar[stage], 0, t.nb * BN + cta * C::kBRows, krow,
-                             0);
+#pragma unroll
+            for (int j = 0; j < NS; ++j)
+              load_b<B_MN, CG>(&map_b, sb + j * C::kBSubBytes, &full_bar[stage], 0,
+                               t.nb * C::kTileN + j * BN + cta * C::kBRows, krow, 0);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -998,7 +1012,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = next_tile(false); tile < total; tile = next_tile(false)) {
-        const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
+        const TileInfo t = decode_tile<CG, NS>(p, s_pref, s_off, s_perm, total0, tile);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -1009,7 +1023,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t ad = da0 + soff, bd = db0 + soff;
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            tc_mma_elect<CG>(d_tmem, ad + k * kStepA, bd + k * kStepB, idesc, (kb | k) != 0);
+#pragma unroll
+            for (int j = 0; j < NS; ++j)   // sub-tile j: accumulator columns [256 j, +256)
+              tc_mma_elect<CG>(d_tmem + j * BN, ad + k * kStepA,
+                               bd + (uint64_t)(j * (C::kBSubBytes >> 4)) + k * kStepB, idesc,
+                               (kb | k) != 0);
           tc_commit_elect<CG>(&empty_bar[stage]);  // frees the smem slot(s) when the MMAs retire
           if (++stage == C::kStages) {
             stage = 0;
@@ -1017,7 +1035,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         tc_commit_elect<CG>(&tfull_bar[acc]);  // accumulator ready for the epilogue(s)
-        if (++acc == 2) {
+        if (++acc == C::kNAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -1033,19 +1051,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool gelu = AUX && p.epilogue == LZ_EPI_GELU, dgelu = AUX && p.epilogue == LZ_EPI_DGELU;
     const bool swiglu = AUX && p.epilogue == LZ_EPI_SWIGLU;
     const bool dswiglu = AUX && p.epilogue == LZ_EPI_DSWIGLU;
-    constexpr int kChunks = BN / kEpiCols / (kEpiWarps / 4);
+    constexpr int kChunks = C::kTileN / kEpiCols / (kEpiWarps / 4);
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = next_tile(false); tile < total; tile = next_tile(false)) {
-      const TileInfo t = decode_tile<CG>(p, s_pref, s_off, s_perm, total0, tile);
+      const TileInfo t = decode_tile<CG, NS>(p, s_pref, s_off, s_perm, total0, tile);
       const int row0 = (p.mode == 0 ? s_off[t.g] : t.g * p.c_grp_rows + p.c_row_off) +
                        t.mb * C::kTileM + cta * BM + quad * 32;
-      const int col0 = t.nb * BN + half * (BN / (kEpiWarps / 4));
+      const int col0 = t.nb * C::kTileN + half * (C::kTileN / (kEpiWarps / 4));
       if (swiglu || dswiglu) {
         swiglu_epilogue(p, swiglu, t, row0, half, lane, tmem_base + ((uint32_t)(quad * 32) << 16) +
                         acc * kAccCols, &tfull_bar[acc], acc_phase, &tempty_bar[acc], wbuf,
                         &map_c, CG);
-        if (++acc == 2) {
+        if (++acc == C::kNAcc) {
           acc = 0;
           acc_phase ^= 1;
         }
@@ -1090,7 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&tfull_bar[acc], acc_phase);
         tc_fence_after();
         const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + acc * kAccCols +
-                               half * (BN / (kEpiWarps / 4));
+                               half * (C::kTileN / (kEpiWarps / 4));
 #pragma unroll 1
         for (int c = 0; c < kChunks; ++c) {
           const int b = c & 1;
@@ -1178,7 +1196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (gelu) plain_tile(std::integral_constant<int, 1>{});
       else if (dgelu) plain_tile(std::integral_constant<int, 2>{});
       else plain_tile(std::integral_constant<int, 0>{});
-      if (++acc == 2) {
+      if (++acc == C::kNAcc) {
         acc = 0;
         acc_phase ^= 1;
       }
@@ -1284,22 +1302,22 @@ extern "C" int lz_gemm_set_cta_group(int cg) {
 }
 extern "C" int lz_gemm_row_align(void) { return BM * g_cta_group; }
 
-template <int A_MN, int B_MN, int CG, bool AUX>
+template <int A_MN, int B_MN, int CG, bool AUX, int NS = 1>
 static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                         const CUtensorMap& mx, const Params& p, const RetMaps& rm, int grid,
                         cudaStream_t s) {
-  auto kern = grouped_gemm_kernel<A_MN, B_MN, CG, AUX>;
+  auto kern = grouped_gemm_kernel<A_MN, B_MN, CG, AUX, NS>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             Cfg<CG, AUX>::kSmemBytes) != cudaSuccess)
+                             Cfg<CG, AUX, NS>::kSmemBytes) != cudaSuccess)
       return lzh::check_launch();
     attr_set = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = Cfg<CG, AUX>::kSmemBytes;
+  cfg.dynamicSmemBytes = Cfg<CG, AUX, NS>::kSmemBytes;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1315,6 +1333,16 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   return lzh::check_launch();
 }
 
+// weight-gradient GEMMs on 256 x 512 tiles (Cfg NS = 2) when N allows; LZ_GEMM_WIDE=0 keeps
+// the 256 x 256 tiles
+static bool wide_wgrad(int N) {
+  static const int on = [] {
+    const char* e = getenv("LZ_GEMM_WIDE");
+    return e ? atoi(e) : 1;
+  }();
+  return on != 0 && N % (2 * BN) == 0;
+}
+
 template <int A_MN, int B_MN, bool AUX>
 static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                            const CUtensorMap& mx, const Params& p, const RetMaps& rm, long tiles,
@@ -1322,6 +1350,14 @@ static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (g_cta_group == 2) {
     long units = tiles < sms / 2 ? tiles : sms / 2;
     if (units < 1) units = 1;
+    if constexpr (!AUX && A_MN == 1) {
+      if (p.mode == 1 && wide_wgrad(p.N)) {
+        const long t2 = tiles / 2;   // 256 x 512 tiles
+        long u2 = t2 < sms / 2 ? t2 : sms / 2;
+        if (u2 < 1) u2 = 1;
+        return launch<A_MN, B_MN, 2, AUX, 2>(ma, mb, mc, mx, p, rm, (int)(2 * u2), s);
+      }
+    }
     return launch<A_MN, B_MN, 2, AUX>(ma, mb, mc, mx, p, rm, (int)(2 * units), s);
   }
   long grid = tiles < sms ? tiles : sms;

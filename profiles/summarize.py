@@ -25,6 +25,10 @@ METRICS = [
     "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
     "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    # L2 side (the GEMMs' bound): bytes through the L2 slices, L2 -> SM
+    # crossbar bytes, L2 throughput vs its peak, and the SM clock the kernel ran at
+    "lts__t_bytes.sum", "l1tex__m_xbar2l1tex_read_bytes.sum",
+    "lts__t_sectors.avg.pct_of_peak_sustained_elapsed", "sm__cycles_elapsed.avg.per_second",
 ]
 
 

@@ -106,8 +106,10 @@ def test_gelu_aux_layout_roundtrip():
 
 
 @pytest.mark.parametrize("sizes,M,N", [([128], 256, 256), ([64, 0, 192, 128], 256, 512),
-                                       ([1024, 512], 1024, 256)])
+                                       ([1024, 512], 1024, 256), ([2048, 0, 4352, 256], 512, 1536),
+                                       ([8192, 3072], 1024, 4096)])
 def test_wgrad_variable_k(sizes, M, N):
+    """Variable-K weight gradients; N % 512 == 0 runs the 256 x 512 tiles (NS = 2)."""
     torch.manual_seed(3)
     off_t, off = _offsets(sizes)
     rows, G = off[-1], len(sizes)
