@@ -489,7 +489,8 @@ __device__ __forceinline__ TileInfo decode_tile(const Params& p, const int32_t* 
   TileInfo t;
   t.remote = false;
   // mode 0: B slices (K x 256 weights per n-block) are the re-read operand
-  const int cb0 = p.mode == 0 ? chunk_blocks(p.l2_chunk_bytes, (long long)p.K * BN * 2, nbn) : 0;
+  const int cb0 =
+      p.mode == 0 ? chunk_blocks(p.l2_chunk_bytes, (long long)p.K * BN * NS * 2, nbn) : 0;
   if (p.mode == 0 && tile < total0) {
     int acc = 0, g = 0;
     for (; g < p.G - 1; ++g) {
@@ -1333,14 +1334,17 @@ static lz_status launch(const CUtensorMap& ma, const CUtensorMap& mb, const CUte
   return lzh::check_launch();
 }
 
-// weight-gradient GEMMs on 256 x 512 tiles (Cfg NS = 2) when N allows; LZ_GEMM_WIDE=0 keeps
-// the 256 x 256 tiles
-static bool wide_wgrad(int N) {
+// 256 x 512 tiles (Cfg NS = 2) for the store-epilogue GEMMs with a long main loop: the
+// weight gradients (K = an expert's rows) and row GEMMs with K >= 2048 (the one-accumulator
+// epilogue is then a few % of a tile); N % 512 == 0.  LZ_GEMM_WIDE=0 keeps 256 x 256, =2
+// only the weight gradients.
+static bool wide_tiles(int mode, int N, int K) {
   static const int on = [] {
     const char* e = getenv("LZ_GEMM_WIDE");
     return e ? atoi(e) : 1;
   }();
-  return on != 0 && N % (2 * BN) == 0;
+  if (on == 0 || N % (2 * BN)) return false;
+  return mode == 1 || (on == 1 && K >= 2048);
 }
 
 template <int A_MN, int B_MN, bool AUX>
@@ -1350,8 +1354,8 @@ static lz_status launch_cg(const CUtensorMap& ma, const CUtensorMap& mb, const C
   if (g_cta_group == 2) {
     long units = tiles < sms / 2 ? tiles : sms / 2;
     if (units < 1) units = 1;
-    if constexpr (!AUX && A_MN == 1) {
-      if (p.mode == 1 && wide_wgrad(p.N)) {
+    if constexpr (!AUX) {
+      if (wide_tiles(p.mode, p.N, p.K)) {
         const long t2 = tiles / 2;   // 256 x 512 tiles
         long u2 = t2 < sms / 2 ? t2 : sms / 2;
         if (u2 < 1) u2 = 1;
