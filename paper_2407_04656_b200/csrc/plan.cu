@@ -77,7 +77,10 @@ __global__ void __launch_bounds__(kSlotThreads) count_kernel(const int32_t* __re
                                                              int32_t* __restrict__ blk_counts,
                                                              int32_t* __restrict__ err) {
   extern __shared__ int32_t s_hist[];
-  pdl_prologue();
+  // wait BEFORE releasing the plan kernel: it then starts with T / R (written before this
+  // kernel) complete and overlaps its table phases with this histogram
+  pdl_wait();
+  pdl_launch_dependents();
   for (int e = threadIdx.x; e < E; e += blockDim.x) s_hist[e] = 0;
   __syncthreads();
   const int b = blockIdx.x;
@@ -163,7 +166,11 @@ struct PlanArgs {
 // shared memory instead of re-reading its own global writes)
 __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   extern __shared__ __align__(16) unsigned char s_raw[];
-  pdl_prologue();
+  // launched behind count_kernel (which waited for its own predecessor before releasing
+  // this grid): T and R are complete; only the final scan needs count_kernel's block
+  // histograms, so the wait for it is deferred to there
+  pdl_launch_dependents();
+  if (a.P == 0) pdl_wait();   // no count_kernel in front: wait for whatever wrote T / R
   const int E = a.E, N = a.N, rank = a.rank;
   int64_t* s_q = reinterpret_cast<int64_t*>(s_raw);
   int32_t* s_M = reinterpret_cast<int32_t*>(s_q + E);  // M[j][e] = sum_i D[i][e][j]
@@ -300,6 +307,7 @@ __global__ void __launch_bounds__(kPlanThreads) plan_kernel(PlanArgs a) {
   }
 
   // -- grid-wide exclusive scan of block histograms, one warp per expert --------
+  pdl_wait();
   if (a.P > 0) scan_block_counts(a.blk_counts, a.blk_base, E, a.B, a.T + rank, N, a.err);
 }
 
