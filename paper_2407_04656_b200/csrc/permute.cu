@@ -235,7 +235,13 @@ __global__ void __launch_bounds__(kRowThreads) combine_kernel(
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
+#ifndef LZ_CBWD_MINB
+#define LZ_CBWD_MINB 2
+#endif
+#ifndef LZ_CBWD_VEC
+#define LZ_CBWD_VEC 4
+#endif
+__global__ void __launch_bounds__(kRowThreads, LZ_CBWD_MINB) combine_bwd_kernel(
     const uint4* __restrict__ dout, const uint4* __restrict__ y, const int32_t* __restrict__ row,
     const int32_t* __restrict__ prank, const unsigned long long* __restrict__ peers_y,
     const unsigned long long* __restrict__ peers_dy,
@@ -264,6 +270,51 @@ __global__ void __launch_bounds__(kRowThreads) combine_bwd_kernel(
 #pragma unroll
     for (int s = 0; s < LZ_MAX_TOPK; ++s) dot[s] = 0.f;
     for (int c0 = lane; c0 < nch; c0 += 32 * kVec) {
+      if (k == 2) {
+        // common top-2: the dout chunk and BOTH expert rows in flight before any math
+        constexpr int kV2 = LZ_CBWD_VEC;
+        uint4 gv[kV2], yv[2][kV2];
+        const uint4* ys[2];
+        uint4* dys[2];
+        float ws[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const long r = __shfl_sync(0xffffffffu, my_row, s);
+          ws[s] = __shfl_sync(0xffffffffu, my_w, s);
+          ys[s] = yrow ? y + (long)__shfl_sync(0xffffffffu, my_yrow, s) * nch
+                       : row_base(const_cast<uint4*>(y), peers_y, my_rk, s) + r * nch;
+          dys[s] = row_base(dy, peers_dy, my_rk, s) + r * nch;
+        }
+        for (int cb = c0; cb < c0 + 32 * kVec; cb += 32 * kV2) {
+#pragma unroll
+          for (int u = 0; u < kV2; ++u) {
+            if (cb + 32 * u < nch) {
+              gv[u] = ld_nc_v4(dout + t * nch + cb + 32 * u);
+              yv[0][u] = ld_nc_v4(ys[0] + cb + 32 * u);
+              yv[1][u] = ld_nc_v4(ys[1] + cb + 32 * u);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kV2; ++u) {
+            if (cb + 32 * u < nch) {
+              float gf[8];
+              bf16x8_to_f32(gv[u], gf);
+#pragma unroll
+              for (int s = 0; s < 2; ++s) {
+                float f[8], o[8];
+                bf16x8_to_f32(yv[s][u], f);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                  dot[s] = fmaf(gf[q], f[q], dot[s]);
+                  o[q] = ws[s] * gf[q];
+                }
+                st_v4(dys[s] + cb + 32 * u, f32_to_bf16x8(o));
+              }
+            }
+          }
+        }
+        continue;
+      }
       float g[kVec][8];
 #pragma unroll
       for (int u = 0; u < kVec; ++u)
