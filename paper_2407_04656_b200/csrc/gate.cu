@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg,
     const float* __restrict__ bias, int Tn, int d, int E, int k, int renorm,
     int32_t* __restrict__ idx, float* __restrict__ w, float* __restrict__ probs,
-    int32_t* __restrict__ hist) {
+    int32_t* __restrict__ hist, int32_t* __restrict__ hist_ws) {
   extern __shared__ __align__(128) uint8_t gs_smem[];
   __shared__ __align__(8) uint64_t full_bar[kGsStages], empty_bar[kGsStages];
   __shared__ __align__(8) uint64_t tfull_bar[kGsTiles], tempty_bar[kGsTiles];
@@ -639,8 +639,39 @@ __global__ void __launch_bounds__(kGsThreads, 1) router_gate_stream(
     }
   }
   __syncthreads();
-  if (threadIdx.x < E && s_hist[threadIdx.x]) atomicAdd(&hist[threadIdx.x], s_hist[threadIdx.x]);
+  // histogram without a memset in front: every CTA stores its 16 counts into its row of a
+  // per-launch workspace slot; the last CTA to arrive (ticket) sums the rows in a fixed
+  // order into hist and resets the ticket for the slot's next use
+  int32_t* ticket = hist_ws;
+  int32_t* rows = hist_ws + 32;
+  if (threadIdx.x < 16) rows[blockIdx.x * 16 + threadIdx.x] = s_hist[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  __shared__ int s_last;
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1) == (int)gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    __shared__ int32_t s_sum[kGsThreads / 16][16];
+    const int e = threadIdx.x & 15, j = threadIdx.x >> 4;   // 22 row groups x 16 experts
+    int32_t v = 0;
+    for (int b = j; b < (int)gridDim.x; b += kGsThreads / 16)
+      v += *reinterpret_cast<volatile int32_t*>(rows + b * 16 + e);
+    s_sum[j][e] = v;
+    __syncthreads();
+    if (threadIdx.x < E) {
+      int32_t tot = 0;
+      for (int jj = 0; jj < kGsThreads / 16; ++jj) tot += s_sum[jj][threadIdx.x];
+      hist[threadIdx.x] = tot;
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+  }
 }
+// per-launch histogram workspaces of the streaming router (ticket + one 16-count row per
+// CTA), a rolling pool: a slot is reused only 256 launches later (also by every replay of a
+// captured graph, whose launch keeps its slot); the ticket self-resets
+constexpr int kGsWsSlots = 256, kGsWsInts = 32 + 256 * 16;
+__device__ int32_t g_gate_ws[kGsWsSlots][kGsWsInts];
 __host__ __device__ constexpr size_t gs_smem_bytes(int d) {
   return (size_t)(kGsStages + 1) * 16 * (d + 8) * 2 +
          (size_t)kGsTiles * kGsMma * 16 * kGsEP * sizeof(float);
@@ -730,7 +761,10 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
       !hist)
     return LZ_ERR_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess) return lzh::check_launch();
+  const bool stream_kernel = E <= 16 && d % 64 == 0 && d <= 1024 && Tn > 0;
+  // the streaming kernel writes the histogram itself (no memset node in front of it)
+  if (!stream_kernel && cudaMemsetAsync(hist, 0, sizeof(int32_t) * E, s) != cudaSuccess)
+    return lzh::check_launch();
   if (Tn == 0) return LZ_OK;
   if (!x || !wg || !idx || !w) return LZ_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(wg)) % 16) return LZ_ERR_ARG;
@@ -738,12 +772,21 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
   const auto* xb = (const __nv_bfloat16*)x;
   const auto* wb = (const __nv_bfloat16*)wg;
   const int NT = (E + 7) / 8;
-  if (E <= 16 && d % 64 == 0 && d <= 1024) {
+  if (stream_kernel) {
     // streaming kernel: one persistent CTA per SM over a contiguous token range (for
     // every Tn, so a token's logits never depend on the batch it came in)
     const size_t smem = gs_smem_bytes(d);
     const int ngroups = (Tn + 15) / 16;
-    const int sgrid = ngroups < lzh::num_sms() ? ngroups : lzh::num_sms();
+    int sgrid = ngroups < lzh::num_sms() ? ngroups : lzh::num_sms();
+    if (sgrid > 256) sgrid = 256;
+    static int32_t* ws_base = nullptr;
+    static unsigned ws_next = 0;
+    if (!ws_base) {
+      void* ptr = nullptr;
+      if (cudaGetSymbolAddress(&ptr, g_gate_ws) != cudaSuccess) return lzh::check_launch();
+      ws_base = (int32_t*)ptr;
+    }
+    int32_t* hist_ws = ws_base + (size_t)(ws_next++ % kGsWsSlots) * kGsWsInts;
 #define LZ_ROUTER_STREAM(n)                                                                 \
   case n: {                                                                                 \
     static bool attr = false;                                                               \
@@ -755,7 +798,7 @@ extern "C" lz_status lz_router_gate(const void* x, const void* wg, const float* 
       attr = true;                                                                          \
     }                                                                                       \
     lzh::launch(router_gate_stream<n>, dim3(sgrid), dim3(kGsThreads), smem, s, 1, xb, wb,  \
-                bias, Tn, d, E, k, renorm, idx, w, probs, hist);                            \
+                bias, Tn, d, E, k, renorm, idx, w, probs, hist, hist_ws);                   \
     break;                                                                                  \
   }
     switch (NT) {
