@@ -22,6 +22,34 @@ def _close(got, ref, rtol=8e-3, atol_scale=1e-3):
     assert (err <= tol).all(), f"max err {err.max().item():.4g} (ref max {ref.abs().max().item():.4g})"
 
 
+def test_router_gate_histogram_slots():
+    """The streaming router writes its histogram without a memset (per-CTA rows in a rolling
+    per-launch workspace slot, summed by the last CTA, ticket self-reset): 600 launches of
+    varying sizes wrap the 256-slot pool twice and every histogram stays exact, also when
+    the same slot is replayed from a CUDA graph."""
+    g = torch.Generator().manual_seed(3)
+    E, k, d = 16, 2, 256
+    wg = (torch.randn(E, d, generator=g) * 0.05).bfloat16().cuda()
+    bias = torch.zeros(E).cuda()
+    xs = [torch.randn(n, d, generator=g).bfloat16().cuda() for n in (1, 17, 700, 5000)]
+    for i in range(600):
+        x = xs[i % len(xs)]
+        idx, _, _, hist = ops.router_gate(x, wg, bias, k)
+        ref = torch.bincount(idx.reshape(-1).long(), minlength=E).int()
+        assert torch.equal(hist, ref), i
+    x = xs[-1]
+    graph = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(graph, stream=s):
+        out = ops.router_gate(x, wg, bias, k)
+    for _ in range(5):
+        out[3].fill_(-1)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out[3], torch.bincount(out[0].reshape(-1).long(), minlength=E).int())
+
+
 @pytest.mark.parametrize("Tn,E,k,renorm", [(1000, 16, 2, False), (4096, 8, 2, True),
                                            (333, 64, 1, False), (64, 5, 3, True),
                                            (100000, 64, 2, False), (5000, 1024, 2, True),
