@@ -134,7 +134,14 @@ class MoELayer(torch.nn.Module):
         # stream while the two weight-gradient GEMMs run (they fill the GEMM tails; cfg2
         # graph replay 6.12 -> 6.04 ms/step at N = 1, tools/tail_ab.py)
         self.tail_overlap = os.environ.get("LZ_TAIL_OVERLAP", "1") != "0"
-        self.tail_overlap_nx = os.environ.get("LZ_TAIL_OVERLAP_NX", "0") == "1"   # N > 1
+        # N > 1: the same reordering (dX GEMM second, dispatch backward + router weight
+        # gradient on the side stream) -- the last expert-gradient all-reduce is then no
+        # longer hidden behind the dX GEMM.  Same-box A/B (tools/step_ab.py): N = 4
+        # 7.79 -> 7.30 ms/step, N = 2 7.09 -> 7.18 (cfg3 37.0 -> 38.0), so "auto" = N >= 4;
+        # LZ_TAIL_OVERLAP_NX=1 / 0 forces it on / off (None = auto, decided per step from the
+        # live world size, so it follows an elastic shrink)
+        nx = os.environ.get("LZ_TAIL_OVERLAP_NX", "auto")
+        self.tail_overlap_nx = None if nx == "auto" else nx == "1"
         # without the tail overlap (N > 1 default), LZ_EARLY_RWGRAD=1: the gate backward right
         # after the combine backward (lz_gate_bwd) and the router weight gradient on a side
         # stream from there (it needs only dlogits and x).  Bit-identical gradients; same-box
@@ -484,7 +491,8 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
         del dret, stage
     _mark(layer, "combine_bwd")
     main = torch.cuda.current_stream(dev)
-    tail = layer.tail_overlap and (mode == "local" or (scatter and layer.tail_overlap_nx))
+    nx = layer.tail_overlap_nx if layer.tail_overlap_nx is not None else N >= 4
+    tail = layer.tail_overlap and (mode == "local" or (scatter and nx))
     early = layer.early_router_wgrad and not tail
     side = None
     if early:

@@ -30,6 +30,8 @@ from paper_2407_04656_b200.placement import plan_for_loads, replica_matrix  # no
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--attr", required=True)
+    ap.add_argument("--values", default="0,1",
+                    help="the two values of the attribute (ints; 0/1 = off/on for switches)")
     ap.add_argument("--config", default="cfg2")
     ap.add_argument("--blocks", type=int, default=8)
     ap.add_argument("--steps", type=int, default=10)
@@ -53,9 +55,12 @@ def main():
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
     x = torch.randn(Tn, d, generator=g, device=dev).bfloat16()
     dout = (torch.randn(Tn, d, generator=g, device=dev) * 1e-2).bfloat16()
+    vals = [int(v) for v in a.values.split(",")]
+    cur = getattr(layer, a.attr)
+    conv = (lambda v: bool(v)) if cur is None or isinstance(cur, bool) else int
     graphs = {}
     for flag in (False, True):
-        setattr(layer, a.attr, flag)
+        setattr(layer, a.attr, conv(vals[int(flag)]))
         gs = GraphedStep(layer, Tn, nbuf=1, backward=True)
         gs.x[0].copy_(x)
         gs.dout[0].copy_(dout)
@@ -88,7 +93,7 @@ def main():
             ms[flag].append(float(t))
     if rank == 0:
         for flag in (False, True):
-            print(f"N={world} {a.config} {a.attr}={int(flag)}: median "
+            print(f"N={world} {a.config} {a.attr}={vals[int(flag)]}: median "
                   f"{statistics.median(ms[flag]):.4f} ms/step  {[round(v, 3) for v in ms[flag]]}")
         print(f"parameter gradients bit-identical: {same}", flush=True)
     if world > 1:
