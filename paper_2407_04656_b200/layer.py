@@ -515,9 +515,9 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
     ov = max(2, (lzh_num_sms() - layer.overlap_reserve)) if N > 1 else 0
     # tail overlap (N = 1): dX GEMM right after the dgrad GEMM; the dispatch backward +
     # router weight gradient (they need only dX, dw and the gate state) then run on a side
-    # stream under the two weight-gradient GEMMs.  N > 1 keeps the dX GEMM last: it hides
-    # the all-reduce of the last expert gradient (~0.33 ms at cfg2, N = 2), which the tail
-    # overlap would expose instead (measured 6.57 vs ~6.1 ms/step at N = 2).
+    # stream under the two weight-gradient GEMMs.  N = 2, 3 keep the dX GEMM last, where it
+    # hides the all-reduce of the last expert gradient, which the tail overlap would expose
+    # instead; from N = 4 the exposed dispatch backward costs more (see tail_overlap_nx).
     if G > 0:
         # dA = dY . W2 (W2_e [d, d_ff] read MN-major), dH = dA * act'(H); on N > 1 the
         # tiles of our own rows start while the other ranks' dY rows arrive
