@@ -570,7 +570,9 @@ def run_gpu(args, cfg):
                          if in_graph else "CUDA events around the GEMM launches of the "
                                           "timed eager steps",
                          "in_graph": in_graph,
-                         "gemms_per_step": gemms_per_step},
+                         "gemms_per_step": gemms_per_step,
+                         "gemm_launches_per_step": (len(in_graph["gemm_launch_ms"])
+                                                    if in_graph else None)},
             "mode": "cuda-graph replay of the whole fwd+bwd step" if graph is not None
                     else "eager (" + graph_err + ")",
             "eager": eager,

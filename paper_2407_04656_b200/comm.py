@@ -167,13 +167,20 @@ class ReplicaGroups:
         for w in self.allreduce_async(grads, local_ids):
             w.wait()
 
-    def allreduce_async(self, grads: Sequence[torch.Tensor], local_ids: Sequence[int]) -> list:
+    def allreduce_async(self, grads: Sequence[torch.Tensor], local_ids: Sequence[int],
+                        id_range: tuple[int, int] | None = None) -> list:
         """As :meth:`allreduce`, issued asynchronously (NCCL streams); returns the works
-        whose ``wait()`` makes the current stream wait for the sums."""
+        whose ``wait()`` makes the current stream wait for the sums.  ``id_range`` = (lo, hi):
+        only experts lo <= e < hi (the same id range on every rank, so every owner set's
+        members issue the same sequence)."""
         works: list = []
         if self.n == 1:
             return works
         for pg, pos in self.buckets(local_ids):
+            if id_range is not None:
+                pos = [q for q in pos if id_range[0] <= local_ids[q] < id_range[1]]
+                if not pos:
+                    continue
             # runs of consecutive EXPERT IDS: every member rank hosts all of them, so they
             # are contiguous local positions on every member and all members issue the same
             # sequence of equally sized in-place all-reduces (no copies)
@@ -198,7 +205,7 @@ HIST = "hist"            # (hist [E] int32)                 -> T [E, N]
 SYNC = "sync"            # ()  every rank's launches so far precede what follows
 BARRIER = "barrier"      # (sym, stream)  device barrier over the exchange buffers
 SYMM = "symm"            # (rows, nbuf, d)                  -> exchange buffers
-EXPERT_AR = "expert_ar"  # (layer, grads)  replica-group sum  -> pending works
+EXPERT_AR = "expert_ar"  # (layer, grads[, (lo, hi) expert ids])  replica-group sum -> works
 WAIT = "wait"            # (works)
 ALLREDUCE = "allreduce"  # (flat tensor)  in-place sum over all ranks
 A2A = "a2a"              # (out, inp, out_splits, in_splits)  row all-to-all-v
@@ -240,8 +247,9 @@ class ProcessFabric:
             dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)   # ranks agree
             return SymmetricRows(self.group, nbuf, int(t.item()), d, device)
         if kind == EXPERT_AR:
-            layer, grads = req[1:]
-            return layer.replica_groups.allreduce_async(grads, layer.local_ids)
+            layer, grads = req[1], req[2]
+            ids = req[3] if len(req) > 3 else None
+            return layer.replica_groups.allreduce_async(grads, layer.local_ids, ids)
         if kind == WAIT:
             for w in req[1]:
                 w.wait()

@@ -148,6 +148,10 @@ class MoELayer(torch.nn.Module):
         # A/B at N = 2 (tools/step_ab.py): 7.07 vs 7.16 and 7.10 vs 7.06 ms/step -- within
         # noise (the side kernel only gets SMs in the persistent GEMMs' tails), so off
         self.early_router_wgrad = os.environ.get("LZ_EARLY_RWGRAD", "0") == "1"
+        # with the tail overlap at N > 1, LZ_SPLIT_WGRAD=1: the last weight-gradient GEMM as two
+        # launches split by expert id, so half of its all-reduce overlaps the other half's
+        # GEMM.  Bit-identical; same-box A/B at N = 4 7.43 -> 7.38 ms/step (within noise): off
+        self.split_last_wgrad = os.environ.get("LZ_SPLIT_WGRAD", "0") == "1"
         self._tail_stream = None
         # exchange buffers: rows = slack x this rank's assignments (+ expert padding); the
         # planner detects a larger need on the device and reserve() grows them
@@ -556,10 +560,23 @@ def _backward_steps(layer: MoELayer, st: dict, x, wg, w1, w2, dout):
         ops.grouped_gemm_wgrad(dH, X, off, dW1)
     if N > 1:
         works += (yield (EXPERT_AR, layer, [dW1])) or []
-    if G > 0:
-        ops.grouped_gemm_wgrad(dY, A, off, dW2, num_sms=ov)
-    if N > 1:
-        works += (yield (EXPERT_AR, layer, [dW2])) or []
+    if N > 1 and tail and layer.split_last_wgrad:
+        # the last expert-gradient all-reduce is exposed with the tail overlap: the dW2 GEMM
+        # runs as two launches split by expert id, so the first half's all-reduce overlaps
+        # the second half's GEMM (same id split on every rank -> same request sequence)
+        half = layer.E // 2
+        ga = sum(1 for e in layer.local_ids if e < half)
+        if ga > 0:
+            ops.grouped_gemm_wgrad(dY, A, off[:ga + 1], dW2[:ga], num_sms=ov)
+        works += (yield (EXPERT_AR, layer, [dW2], (0, half))) or []
+        if G - ga > 0:
+            ops.grouped_gemm_wgrad(dY, A, off[ga:], dW2[ga:], num_sms=ov)
+        works += (yield (EXPERT_AR, layer, [dW2], (half, layer.E))) or []
+    else:
+        if G > 0:
+            ops.grouped_gemm_wgrad(dY, A, off, dW2, num_sms=ov)
+        if N > 1:
+            works += (yield (EXPERT_AR, layer, [dW2])) or []
     if not tail:
         if G > 0:
             if scatter:

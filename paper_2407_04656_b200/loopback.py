@@ -189,8 +189,9 @@ class LoopbackWorld:
             layers = {r: reqs[r][1] for r in ranks}
             grads = {r: reqs[r][2] for r in ranks}
             E = layers[ranks[0]].E
+            lo, hi = reqs[ranks[0]][3] if len(reqs[ranks[0]]) > 3 else (0, E)
             for gi in range(len(grads[ranks[0]])):
-                for e in range(E):
+                for e in range(lo, hi):
                     owners = [(r, layers[r].local_ids.index(e)) for r in ranks
                               if e in layers[r].local_ids]
                     if len(owners) < 2:

@@ -87,6 +87,14 @@ def _worker(rank, n, port, q):
             want = sum(j + 1 for j in owners)
             assert torch.allclose(g1[p], torch.full((3, 2), float(want * (e + 1))))
             assert torch.allclose(g2[p], torch.full((2,), float(want)))
+        # the same sums issued as two expert-id ranges (the split last weight-gradient
+        # all-reduce of the backward tail): every owner set's members issue the same sequence
+        h1 = torch.stack([torch.full((3, 2), float(rank + 1) * (e + 1)) for e in local])
+        works = groups.allreduce_async([h1], local, (0, E // 2))
+        works += groups.allreduce_async([h1], local, (E // 2, E))
+        for w in works:
+            w.wait()
+        assert torch.equal(h1, g1)
         q.put((rank, "ok"))
     except Exception as exc:  # surface to the parent
         import traceback

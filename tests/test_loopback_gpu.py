@@ -100,23 +100,25 @@ def _inputs(N, Tn, d, seed=11):
     return xs, douts
 
 
-# tail: the N > 1 variant of the backward tail overlap (LZ_TAIL_OVERLAP_NX=1; off by default)
-@pytest.mark.parametrize("N,E,k,act,zipf,exchange,scatter,tail", [
-    (2, 16, 2, "gelu", 1.2, "p2p", True, False),      # the product default at N > 1
-    (4, 16, 2, "swiglu", 1.2, "p2p", True, False),
-    (8, 16, 2, "gelu", 1.2, "p2p", True, False),
-    (8, 64, 1, "gelu", 1.5, "p2p", True, True),       # cfg4-like: 64 experts, top-1
-    (4, 64, 2, "swiglu", 0.8, "p2p", True, False),
-    (3, 8, 2, "gelu", 0.0, "p2p", True, True),        # side-stream backward tail at N > 1
-    (4, 16, 2, "gelu", 1.2, "p2p", False, False),     # gathering P2P (LZ_P2P_SCATTER=0)
-    (4, 16, 2, "gelu", 1.2, "nccl", True, False),     # LZ_EXCHANGE=nccl: a2a-v + regroup
-    (2, 8, 2, "swiglu", 2.5, "nccl", True, False),
+# tail: the N > 1 variant of the backward tail overlap (LZ_TAIL_OVERLAP_NX; None = the
+# default "auto": on from N = 4); split: the last weight-gradient GEMM + all-reduce in two
+# expert-id halves (LZ_SPLIT_WGRAD=1)
+@pytest.mark.parametrize("N,E,k,act,zipf,exchange,scatter,tail,split", [
+    (2, 16, 2, "gelu", 1.2, "p2p", True, None, False),      # the product default, N = 2
+    (4, 16, 2, "swiglu", 1.2, "p2p", True, None, False),    # the product default, N = 4
+    (8, 16, 2, "gelu", 1.2, "p2p", True, False, False),
+    (8, 64, 1, "gelu", 1.5, "p2p", True, None, True),       # cfg4-like: 64 experts, top-1
+    (4, 64, 2, "swiglu", 0.8, "p2p", True, False, False),
+    (3, 8, 2, "gelu", 0.0, "p2p", True, True, True),        # side-stream backward tail at N = 3
+    (4, 16, 2, "gelu", 1.2, "p2p", False, False, False),    # gathering P2P (LZ_P2P_SCATTER=0)
+    (4, 16, 2, "gelu", 1.2, "nccl", True, False, False),    # LZ_EXCHANGE=nccl: a2a-v + regroup
+    (2, 8, 2, "swiglu", 2.5, "nccl", True, False, False),
 ])
-def test_loopback_fwd_bwd_matches_oracle(N, E, k, act, zipf, exchange, scatter, tail):
+def test_loopback_fwd_bwd_matches_oracle(N, E, k, act, zipf, exchange, scatter, tail, split):
     d, dff, Tn = 512, 1024, 512
     world, layers, R = _world(N, E, k, d, dff, act, zipf, exchange=exchange)
     for L in layers:
-        L.scatter, L.tail_overlap_nx = scatter, tail
+        L.scatter, L.tail_overlap_nx, L.split_last_wgrad = scatter, tail, split
     xs, douts = _inputs(N, Tn, d)
     outs, grads = world.step(layers, xs, douts)
     torch.cuda.synchronize()
