@@ -69,6 +69,7 @@ def main():
     K, MN = _lib.LZ_K_MAJOR, _lib.LZ_MN_MAJOR
     # name: (mode, A, B, C, aux, M, N, K, b_major, epilogue)
     cases = {
+        "fwd1 store": (0, X, W1, H, None, 0, f1, d, K, _lib.LZ_EPI_STORE),
         "fwd1+act": (0, X, W1, A, H, 0, f1, d, K, act),
         "fwd2": (0, A, W2, Y, None, 0, d, dff, K, _lib.LZ_EPI_STORE),
         "dgrad2+dact": (0, dY, W2, dA, H, 0, dff, d, MN, dact),
