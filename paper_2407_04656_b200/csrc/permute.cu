@@ -777,28 +777,44 @@ __global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restri
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(r2_smem);
   // B fragments of the step: [kg][n][h][hi / lo][32 lanes]
   uint32_t* s_bf = reinterpret_cast<uint32_t*>(r2_smem + kR2Stages * kR2StageBytes);
-  // staging: kR2Tok rows x 256 B of x (16 pieces of 16 B per row) + kR2Tok x 16 dlogits
+  // staging: kR2Tok rows x 256 B of x (16 pieces of 16 B per row) + kR2Tok x 16 dlogits.
+  // Thread tid copies piece (tid & 15) of rows (tid >> 4) + 8 j: its global / shared
+  // addresses advance by fixed strides, precomputed once
+  const int ti0 = threadIdx.x >> 4, cc0 = threadIdx.x & 15;
+  const __nv_bfloat16* xg0 = x + (t_begin + ti0) * d + cbase + cc0 * 8;
+  const uint32_t sx_off = (uint32_t)((ti0 * kR2Row + cc0 * 8) * 2);
+  // dlogits: one 16-byte piece (4 experts) per thread when a token's 16-expert slice is
+  // 16-byte aligned (E % 4 == 0), else 4-byte copies
+  const bool dl16 = (E % 4) == 0;
+  const int dti = threadIdx.x >> 2, dq = threadIdx.x & 3;   // 32 tokens x 4 pieces
   auto stage = [&](int buf, long tt) {
     const uint32_t sx = sbase + (uint32_t)(buf * kR2StageBytes);
+    const long rel = tt - t_begin;
+    const __nv_bfloat16* xg = xg0 + rel * d;
 #pragma unroll
-    for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
-      const int q = threadIdx.x + j * 128;
-      const int ti = q >> 4, cc = q & 15;
-      const long t = tt + ti;
-      const bool ok = t < t_end;
-      cp_async16(sx + (uint32_t)((ti * kR2Row + cc * 8) * 2), x + (ok ? t : 0) * d + cbase + cc * 8,
+    for (int j = 0; j < kR2Tok / 8; ++j) {
+      const bool ok = tt + ti0 + 8 * j < t_end;
+      cp_async16(sx + sx_off + (uint32_t)(8 * j * kR2Row * 2), ok ? (const void*)(xg + 8L * j * d)
+                                                                 : (const void*)x,
                  ok);
     }
     const uint32_t sdl = sx + (uint32_t)(kR2Tok * kR2Row * 2);
+    if (dl16) {
+      const long t = tt + dti;
+      const bool ok = t < t_end && e0 + 4 * dq < E;
+      cp_async16(sdl + (uint32_t)((dti * 16 + 4 * dq) * 4),
+                 ok ? (const void*)(dlog + t * E + e0 + 4 * dq) : (const void*)dlog, ok);
+    } else {
 #pragma unroll
-    for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
-      const int q = threadIdx.x + j * 128;
-      const int ti = q >> 4, ei = q & 15;
-      const long t = tt + ti;
-      const bool ok = t < t_end && e0 + ei < E;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sdl + (uint32_t)(q * 4)),
-                   "l"(dlog + (ok ? t * E + e0 + ei : 0)), "r"(ok ? 4 : 0)
-                   : "memory");
+      for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
+        const int q = threadIdx.x + j * 128;
+        const int ti = q >> 4, ei = q & 15;
+        const long t = tt + ti;
+        const bool ok = t < t_end && e0 + ei < E;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sdl + (uint32_t)(q * 4)),
+                     "l"(dlog + (ok ? t * E + e0 + ei : 0)), "r"(ok ? 4 : 0)
+                     : "memory");
+      }
     }
   };
   float acc[2][2][4];
@@ -839,9 +855,12 @@ __global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restri
       s_bf[(((kg * 2 + bn) * 2 + bh) * 2 + 0) * 32 + lane] = hi;
       s_bf[(((kg * 2 + bn) * 2 + bh) * 2 + 1) * 32 + lane] = bf16pair(v0 - h0, v1 - h1);
     }
-    if (blockIdx.y == 0 && threadIdx.x < 16) {
-#pragma unroll 8
-      for (int ti = 0; ti < kR2Tok; ++ti) bacc += dl[ti * 16 + threadIdx.x];
+    if (blockIdx.y == 0) {
+      // bias partial: thread (expert e = tid & 15, token group j = tid >> 4) adds its 4 of
+      // the step's 32 tokens (all 128 threads, no serial 32-token loop in one warp)
+      const int e = threadIdx.x & 15, j = threadIdx.x >> 4;
+#pragma unroll
+      for (int q = 0; q < kR2Tok / 8; ++q) bacc += dl[(j * (kR2Tok / 8) + q) * 16 + e];
     }
     __syncthreads();   // B fragments of step i visible
 #pragma unroll
@@ -890,8 +909,18 @@ __global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restri
       }
     }
   }
-  if (blockIdx.y == 0 && threadIdx.x < 16 && e0 + threadIdx.x < E)
-    part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = bacc;
+  if (blockIdx.y == 0) {
+    // the 8 token-group partials of each expert, summed in a fixed order
+    __shared__ float s_b[8][16];
+    s_b[threadIdx.x >> 4][threadIdx.x & 15] = bacc;
+    __syncthreads();
+    if (threadIdx.x < 16 && e0 + threadIdx.x < E) {
+      float v = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v += s_b[j][threadIdx.x];
+      part_bias[(long)blockIdx.x * E + e0 + threadIdx.x] = v;
+    }
+  }
 }
 
 // Block = 8 warps x 32 consecutive output elements (coalesced 128-byte loads); warp w
