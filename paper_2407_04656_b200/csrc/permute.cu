@@ -750,15 +750,23 @@ __global__ void __launch_bounds__(256, 2) router_wgrad_partial(const float* __re
 
 // Column-sliced tensor-core variant (the default for d % 128 == 0): block (r, c, z) reduces
 // token range r for the 128 columns [128 c, +128) and experts [16 z, +16); warp w owns 32
-// of the columns (two m16 tiles), so the accumulators are 32 registers and 8 blocks fit an
-// SM.  The token ranges are few (~8 * SMs / slices), so the partials are E * d * 4 bytes
-// per range (cfg2: 9.7 MB).  Per 16-token step the block stages 16 x 128 bf16 of x and the
-// 16 x 16 dlogits through a cp.async ring; the dlogits' hi / lo bf16 B fragments are built
-// once per step by the whole block into shared memory.
-constexpr int kR2Cols = 128, kR2Row = kR2Cols + 8, kR2Stages = 3, kR2Tok = 32;
+// of the columns (two m16 tiles), so the accumulators are 32 registers.  The token ranges
+// are few (blocks per SM * SMs / slices), so the partials are E * d * 4 bytes per range
+// (cfg2: 3.6 MB).  Per step the block stages kR2Tok x 128 bf16 of x and the kR2Tok x 16
+// dlogits through a cp.async ring (precomputed strided addresses); the dlogits' hi / lo
+// bf16 B fragments are built once per step by the whole block into shared memory, and the
+// bias partial is summed by all threads.
+// 64-token steps, 3 stages, 3 blocks per SM: measured best of (32|64|96|128 tokens) x
+// (2..4 stages) x (1..6 blocks/SM) -- 30.0 us vs 32.1 us for 32-token steps at 6 blocks/SM
+#ifndef LZ_R2_TOK
+#define LZ_R2_TOK 64
+#define LZ_R2_ST 3
+#define LZ_R2_BLK 3
+#endif
+constexpr int kR2Cols = 128, kR2Row = kR2Cols + 8, kR2Stages = LZ_R2_ST, kR2Tok = LZ_R2_TOK;
 constexpr int kR2StageBytes = kR2Tok * kR2Row * 2 + kR2Tok * 16 * 4;   // x tile + dlogits
 constexpr int kR2Smem = kR2Stages * kR2StageBytes + (kR2Tok / 16) * 2 * 2 * 2 * 32 * 4;
-__global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restrict__ dlog,
+__global__ void __launch_bounds__(128, LZ_R2_BLK) router_wgrad_tc2(const float* __restrict__ dlog,
                                                          const __nv_bfloat16* __restrict__ x,
                                                          int Tn, int d, int E,
                                                          float* __restrict__ part,
@@ -800,10 +808,13 @@ __global__ void __launch_bounds__(128, 6) router_wgrad_tc2(const float* __restri
     }
     const uint32_t sdl = sx + (uint32_t)(kR2Tok * kR2Row * 2);
     if (dl16) {
-      const long t = tt + dti;
-      const bool ok = t < t_end && e0 + 4 * dq < E;
-      cp_async16(sdl + (uint32_t)((dti * 16 + 4 * dq) * 4),
-                 ok ? (const void*)(dlog + t * E + e0 + 4 * dq) : (const void*)dlog, ok);
+#pragma unroll
+      for (int jj = 0; jj < kR2Tok / 32; ++jj) {
+        const long t = tt + dti + 32 * jj;
+        const bool ok = t < t_end && e0 + 4 * dq < E;
+        cp_async16(sdl + (uint32_t)(((dti + 32 * jj) * 16 + 4 * dq) * 4),
+                   ok ? (const void*)(dlog + t * E + e0 + 4 * dq) : (const void*)dlog, ok);
+      }
     } else {
 #pragma unroll
       for (int j = 0; j < kR2Tok * 16 / 128; ++j) {
@@ -1209,7 +1220,7 @@ static bool wgrad_tc(int d) { return d % kR2Cols == 0; }
 static int wgrad_nblk(int Tn, int d, int E) {
   if (wgrad_tc(d)) {
     const int slices = (d / kR2Cols) * ((E + 15) / 16);
-    int n = (6 * lzh::num_sms() + slices - 1) / slices;
+    int n = (LZ_R2_BLK * lzh::num_sms() + slices - 1) / slices;
     const int steps = (Tn + kR2Tok - 1) / kR2Tok;
     if (n > steps) n = steps;
     return n < 1 ? 1 : n;
@@ -1242,6 +1253,13 @@ extern "C" lz_status lz_router_wgrad(const float* dlogits, const void* x, int Tn
   float* part_bias = part + (size_t)nblk * E * d;
   if (wgrad_tc(d)) {
     dim3 grid(nblk, d / kR2Cols, (E + 15) / 16);
+    static bool attr2 = false;
+    if (!attr2 && kR2Smem > 48 * 1024) {
+      if (cudaFuncSetAttribute(router_wgrad_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               kR2Smem) != cudaSuccess)
+        return lzh::check_launch();
+      attr2 = true;
+    }
     lzh::launch(router_wgrad_tc2, grid, dim3(128), kR2Smem, s, 1, dlogits,
                 (const __nv_bfloat16*)x, Tn, d, E, part, part_bias);
   } else {
