@@ -465,10 +465,19 @@ __global__ void __launch_bounds__(32 * kRouterWarps, 2) router_gate_pipe(
 // The register-direct kernel below needs 2 waves of 16-token warps at 64K tokens, each
 // warp latency-bound on 4 KB in flight.
 // ---------------------------------------------------------------------------
-constexpr int kGsMma = 4;         // MMA (column-split) warps
-constexpr int kGsFin = 6;         // finisher warps
-constexpr int kGsStages = 4;      // x ring depth
-constexpr int kGsTiles = 12;      // partial-logit tiles
+// warp / ring shape of the streaming router: (MMA warps, finisher warps, stages, tiles) =
+// (4, 6, 4, 12); measured against (8, 6, 4, 6), (4, 8, 4, 12), (8, 4, 4, 6), (4, 6, 3, 12):
+// all within 28.8-29.9 us at cfg2 -- the kernel is bound by its fixed per-launch costs
+#ifndef LZ_GS_MMA
+#define LZ_GS_MMA 4
+#define LZ_GS_FIN 6
+#define LZ_GS_STAGES 4
+#define LZ_GS_TILES 12
+#endif
+constexpr int kGsMma = LZ_GS_MMA;         // MMA (column-split) warps
+constexpr int kGsFin = LZ_GS_FIN;         // finisher warps
+constexpr int kGsStages = LZ_GS_STAGES;   // x ring depth
+constexpr int kGsTiles = LZ_GS_TILES;     // partial-logit tiles
 constexpr int kGsEP = 17;         // padded partial row (16 experts + 1)
 constexpr int kGsThreads = 32 * (kGsMma + kGsFin + 1);
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
