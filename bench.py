@@ -357,6 +357,11 @@ def run_gpu(args, cfg):
             return h0.elapsed_time(h1)
 
         ms_graph_e2e = timed_e2e(False)
+        # the GEMMs timed from inside the graph: slot 2 carries event-record nodes around
+        # the step and every grouped-GEMM launch; each replay is read back, so the GEMM
+        # time and the step time come from the same replays (measured before the secondary
+        # e2e variant, so the board is in the same state as in round 2a's order)
+        rt = graph.replay_times(args.steps)
         ms_graph_e2e_dout = timed_e2e(True) if cfg["bwd"] else None
         for b in range(2):
             graph.dout[b].copy_(dout)
@@ -366,10 +371,6 @@ def run_gpu(args, cfg):
             ms_graph, ms_graph_e2e, ms_graph_e2e_dout = (float(v) for v in t.tolist())
             if not cfg["bwd"]:
                 ms_graph_e2e_dout = None
-        # the GEMMs timed from inside the graph: slot 2 carries event-record nodes around
-        # the step and every grouped-GEMM launch; each replay is read back, so the GEMM
-        # time and the step time come from the same replays
-        rt = graph.replay_times(args.steps)
         in_graph = {"step_ms": float(np.median(rt["step_ms"])),
                     "gemm_ms": float(np.median(rt["gemm_ms"])),
                     "gemm_launch_ms": [float(np.median(c)) for c in zip(*rt["gemm_launch_ms"])]}
